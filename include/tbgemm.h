@@ -1,0 +1,141 @@
+/*
+ * tbgemm.h — C-ABI of the B200-native GEMM hot path (libtbgemm.so).
+ *
+ * This is the drop-in boundary for the reference's GEMM operator interface.
+ * The reference (tunedblas, pure Python/NumPy) has no FFI of its own; its
+ * internal operator call is
+ *     run_kernel(family, config, args, ctx, precision)
+ *         pkg/src/tunedblas/kernels/compute.py:116-130
+ * with GemmIndirectArgs / GemmDirectArgs (compute.py:80-113) carrying padded
+ * NumPy workspaces and slice closures, driven from
+ *     _gemm_on_arrays   pkg/src/tunedblas/routines/level3.py:48-91
+ *     _gemm_batched_core pkg/src/tunedblas/routines/extras.py:188-286
+ * Those carry NumPy arrays and closures and cannot cross a C boundary, so the
+ * cut sits just below the routine layer's validation (level3.py:94-133,
+ * extras.py:188-348): every argument check happens in the Python host layer
+ * (identical error types and text), and these entry points receive plain
+ * device pointers, element offsets and leading dimensions — the unpadded
+ * operands, exactly as the routine's Buffer views describe them.
+ *
+ * Conventions
+ *   - All pointers (a, b, c and the batched arrays) are DEVICE pointers.
+ *   - Offsets, leading dimensions and strides are in ELEMENTS.
+ *   - Layout/transpose follow the reference enums (core.py:105-117); for the
+ *     real precisions CONJUGATE == TRANS (level3.py:135-146).
+ *   - Semantics per element: S computes in FP32 with a
+ *     sequential-k FMA chain; H reads FP16, accumulates FP32 on the tensor
+ *     cores and rounds once (RNE) to FP16.  Epilogue = alpha*acc, or
+ *     alpha*acc + beta*C as three separately rounded FP32 ops (compute.py:
+ *     408-412).  beta == 0 never reads C; alpha == 0 or k == 0 never reads
+ *     A or B (level3.py:125-132).
+ *   - Calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy).
+ *   - Return value: TB_OK or a TB_ERR_* status; tb_status_str() explains it.
+ *     Argument errors are the host layer's job; the library returns
+ *     TB_ERR_INVALID only as a last line of defence.
+ */
+#ifndef TBGEMM_H_
+#define TBGEMM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TBGEMM_ABI_VERSION 1
+
+/* Precision.H / Precision.S   (core.py:43-50) */
+enum { TB_PREC_H = 0, TB_PREC_S = 1 };
+/* Layout.ROW_MAJOR / COL_MAJOR (core.py:105-107) */
+enum { TB_COL_MAJOR = 0, TB_ROW_MAJOR = 1 };
+/* Transpose.NO / YES / CONJUGATE (core.py:110-113) */
+enum { TB_NO_TRANS = 0, TB_TRANS = 1, TB_CONJ_TRANS = 2 };
+
+/* Status codes. */
+enum {
+  TB_OK = 0,
+  TB_ERR_INVALID = 1,      /* argument rejected by the library */
+  TB_ERR_CUDA = 2,         /* CUDA runtime / launch failure */
+  TB_ERR_UNSUPPORTED = 3,  /* e.g. no sm_100a device, TF32 flag on H */
+  TB_ERR_DRIVER = 4        /* cuTensorMapEncodeTiled unavailable/failed */
+};
+
+/* Flags (bitwise OR). */
+enum {
+  TB_FLAG_NONE = 0,
+  TB_FLAG_TF32 = 1,        /* opt-in TF32 tensor-core SGEMM (separate tolerance) */
+  TB_FLAG_NO_TMA = 2,      /* HGEMM: force the LDG producer (testing)          */
+  TB_FLAG_SIMT_GENERAL = 4 /* SGEMM: force the general predicated kernel        */
+};
+
+/*
+ * The 14 reference tuning parameters (GemmParams, params.py:120-146) in the
+ * reference's order.  The library maps them onto its nearest sm_100a
+ * instantiation (DESIGN.md §"Parameter mapping"); NULL = built-in default.
+ */
+typedef struct tb_gemm_params {
+  int32_t MWG, NWG, KWG, MDIMC, NDIMC, MDIMA, NDIMB, KWI, VWM, VWN, STRM, STRN,
+      SA, SB;
+} tb_gemm_params;
+
+/*
+ * What the last call on this thread launched (engine.py:128-133 records a
+ * LaunchRecord; this is its device-side counterpart).
+ */
+typedef struct tb_launch_record {
+  char kernel[64];         /* instantiation name, e.g. "hgemm_tc_tma_128x256" */
+  int64_t grid[3];
+  int32_t block[3];
+  int32_t cluster[3];
+  int32_t smem_bytes;
+  int32_t launches;        /* kernels launched by the last call (0 = none) */
+  int64_t tiles;           /* output tiles (x batch) the launch covers     */
+} tb_launch_record;
+
+/* C = alpha*op(A)*op(B) + beta*C   — replaces level3.py:48-91 → compute.py:384-471 */
+int tb_gemm(int prec, int layout, int trans_a, int trans_b, int64_t m,
+            int64_t n, int64_t k, float alpha, const void* a, int64_t a_off,
+            int64_t lda, const void* b, int64_t b_off, int64_t ldb,
+            float beta, void* c, int64_t c_off, int64_t ldc,
+            const tb_gemm_params* params, int flags, void* stream);
+
+/* Instance i uses base offset + i*stride — replaces extras.py:309-348 → 188-286 */
+int tb_gemm_strided_batched(int prec, int layout, int trans_a, int trans_b,
+                            int64_t m, int64_t n, int64_t k, float alpha,
+                            const void* a, int64_t a_off, int64_t lda,
+                            int64_t stride_a, const void* b, int64_t b_off,
+                            int64_t ldb, int64_t stride_b, float beta, void* c,
+                            int64_t c_off, int64_t ldc, int64_t stride_c,
+                            int64_t batch, const tb_gemm_params* params,
+                            int flags, void* stream);
+
+/*
+ * Per-instance offsets and scalars — replaces extras.py:289-306 → 188-286.
+ * alphas/betas (float32) and a_offs/b_offs/c_offs (int64) are DEVICE arrays
+ * of length `batch`.  `offs_aligned` != 0 asserts every offset is a multiple
+ * of 8 elements (H) / 4 elements (S) so vector loads may be used.
+ */
+int tb_gemm_batched(int prec, int layout, int trans_a, int trans_b, int64_t m,
+                    int64_t n, int64_t k, const float* alphas, const void* a,
+                    const int64_t* a_offs, int64_t lda, const void* b,
+                    const int64_t* b_offs, int64_t ldb, const float* betas,
+                    void* c, const int64_t* c_offs, int64_t ldc, int64_t batch,
+                    int offs_aligned, const tb_gemm_params* params, int flags,
+                    void* stream);
+
+/* Fill the record of the last launch issued from the calling thread. */
+int tb_last_launch(tb_launch_record* out);
+/* Human-readable text for a status code (static storage). */
+const char* tb_status_str(int status);
+/* Text of the last CUDA error seen by the library on this thread. */
+const char* tb_last_error(void);
+/* TBGEMM_ABI_VERSION of the loaded library. */
+int tb_abi_version(void);
+/* Number of SMs on the current device (0 if no device). */
+int tb_device_sm_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TBGEMM_H_ */

@@ -1,0 +1,313 @@
+// hgemm_tc.cuh — FP16 GEMM on the 5th-gen tensor cores (tcgen05 + TMEM).
+//
+// Replaces the reference's indirect Xgemm path for Precision.H
+// (pkg/src/tunedblas/routines/level3.py:48-91 → compute.py:384-420): the
+// pad / transpose / copy pre-kernels (level3.py:71-82, 134-147) disappear —
+// TMA tensor maps read the UNPADDED operands in whatever major-ness the
+// caller's layout/trans flags imply (OOB boxes zero-fill), and the
+// unpad + single FP16 rounding (level3.py:91) is fused into the epilogue.
+//
+// Persistent, warp-specialised kernel (one CTA per SM):
+//   producer  : TMA (one elected thread) or, when operands are not 16-B
+//               aligned / offsets are per-instance, 4 warps of predicated
+//               LDG + swizzled STS into the identical smem layout;
+//   MMA       : one thread issues tcgen05.mma.cta_group::1.kind::f16
+//               (M=128, N=BN, K=16) into a double-buffered FP32 TMEM
+//               accumulator (2 x BN columns);
+//   epilogue  : 4 warps, tcgen05.ld 32x32b → FP32 alpha/beta epilogue
+//               (Epi: three separately rounded ops) → RNE to FP16 → global.
+// Pipelines: smem full/empty mbarrier ring (STAGES deep), TMEM full/empty
+// pair; tiles are visited in grouped raster order (tile_coords).
+//
+// Both producers fill byte-identical shared memory and the MMA sequence per
+// output element (K in 64-deep blocks of 4 x K16 steps, zero-filled tail)
+// is the same, so every HGEMM path — TMA or LDG, single or batched — gives
+// bitwise-identical results for the same (m, n, k).
+#pragma once
+
+#include "common.cuh"
+#include "sgemm_simt.cuh"  // tile_coords
+
+namespace tb {
+
+constexpr int HG_BM = 128;
+constexpr int HG_BK = 64;  // 64 halves = 128 B = one SW128 row
+
+template <int BN, bool TMA>
+struct HgCfg {
+  static constexpr int STAGES = (BN >= 256) ? 4 : 6;
+  static constexpr int A_BYTES = HG_BM * HG_BK * 2;            // 16 KB
+  static constexpr int B_BYTES = BN * HG_BK * 2;               // 8/16/32 KB
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
+                                  : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int PROD_WARPS = TMA ? 1 : 4;
+  static constexpr int MMA_WARP = TMA ? 1 : 4;
+  static constexpr int ALLOC_WARP = TMA ? 2 : 5;
+  static constexpr int EPI_WARP0 = TMA ? 4 : 8;
+  static constexpr int THREADS = (EPI_WARP0 + 4) * 32;
+  static constexpr int BAR_BYTES = 1024;
+  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES;
+};
+
+// Swizzle-128B placement of 16-byte chunk `c` (0..7) of 128-byte row `r`
+// inside a 1024-byte-aligned region (identical to what TMA SWIZZLE_128B writes).
+__device__ __forceinline__ uint32_t sw128_off(int r, int c) {
+  return static_cast<uint32_t>((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
+}
+
+// Load 8 consecutive halves along the operand's contiguous dimension,
+// zero-filling past `valid` elements.
+template <bool VEC>
+__device__ __forceinline__ uint4 ldg_chunk8(const __half* src, int valid) {
+  if (VEC && valid >= 8) return __ldg(reinterpret_cast<const uint4*>(src));
+  uint16_t h[8];
+  const uint16_t* s16 = reinterpret_cast<const uint16_t*>(src);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) h[q] = (q < valid) ? __ldg(s16 + q) : static_cast<uint16_t>(0);
+  uint4 r;
+  r.x = h[0] | (static_cast<uint32_t>(h[1]) << 16);
+  r.y = h[2] | (static_cast<uint32_t>(h[3]) << 16);
+  r.z = h[4] | (static_cast<uint32_t>(h[5]) << 16);
+  r.w = h[6] | (static_cast<uint32_t>(h[7]) << 16);
+  return r;
+}
+
+// LDG producer for one operand tile of ROWS (M or N) x 64 (K):
+//   K-major  (!MN): smem = ROWS rows of 128 B (row = M/N index, chunk = K/8)
+//   MN-major ( MN): ROWS/64 sub-tiles of 64 K-rows x 128 B (chunk = MN/8)
+// `base` points at the operand element (mn0, k0) of this instance; `ld` is
+// the stride of the non-contiguous dimension.
+template <int ROWS, bool MN, bool VEC>
+__device__ __forceinline__ void ldg_fill_tile(uint8_t* smem, const __half* base, int64_t ld,
+                                              int mn_left, int k_left, int tid) {
+  constexpr int CHUNKS = ROWS * 8;
+  constexpr int PER_T = CHUNKS / 128;
+  uint4 v[PER_T];
+#pragma unroll
+  for (int j = 0; j < PER_T; ++j) {
+    const int g = tid + j * 128;
+    if (!MN) {
+      const int r = g >> 3, c = g & 7;       // r: M/N row, c: K chunk
+      const int valid = (r < mn_left) ? min(8, k_left - c * 8) : 0;
+      v[j] = (valid > 0) ? ldg_chunk8<VEC>(base + static_cast<int64_t>(r) * ld + c * 8, valid)
+                         : make_uint4(0, 0, 0, 0);
+    } else {
+      const int sub = g >> 9, r = (g >> 3) & 63, c = g & 7;  // r: K row, c: MN chunk
+      const int mn = sub * 64 + c * 8;
+      const int valid = (r < k_left) ? min(8, mn_left - mn) : 0;
+      v[j] = (valid > 0) ? ldg_chunk8<VEC>(base + static_cast<int64_t>(r) * ld + mn, valid)
+                         : make_uint4(0, 0, 0, 0);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < PER_T; ++j) {
+    const int g = tid + j * 128;
+    uint32_t off;
+    if (!MN) {
+      off = sw128_off(g >> 3, g & 7);
+    } else {
+      off = (g >> 9) * 8192 + sw128_off((g >> 3) & 63, g & 7);
+    }
+    *reinterpret_cast<uint4*>(smem + off) = v[j];
+  }
+}
+
+template <int BN, bool TMA, bool A_MN, bool B_MN, bool VEC>
+__global__ void __launch_bounds__(HgCfg<BN, TMA>::THREADS, 1)
+    hgemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    Problem p, int tiles_m, int tiles_n, int group_m, int64_t total_tiles) {
+  using C = HgCfg<BN, TMA>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], TMA ? 1 : 128);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_mbar_init();
+  }
+  if (TMA && warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == C::ALLOC_WARP) tmem_alloc(tmem_holder, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int nkb = static_cast<int>((p.k + HG_BK - 1) / HG_BK);
+
+  if (warp < C::PROD_WARPS) {
+    // ======================= producer =======================
+    int s = 0;
+    uint32_t ph = 0;
+    if (TMA) {
+      if (lane == 0) {
+        for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+          int64_t z; int mt, nt;
+          tile_coords(t, tiles_m, tiles_n, group_m, z, mt, nt);
+          const int m0 = mt * HG_BM, n0 = nt * BN, zz = static_cast<int>(z);
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(&empty[s], ph ^ 1);
+            mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+            const int k0 = kb * HG_BK;
+            uint8_t* a_dst = sA + s * C::A_BYTES;
+            uint8_t* b_dst = sB + s * C::B_BYTES;
+            if (!A_MN) {
+              tma_load_3d(a_dst, &tmA, &full[s], k0, m0, zz);
+            } else {
+              tma_load_3d(a_dst, &tmA, &full[s], m0, k0, zz);
+              tma_load_3d(a_dst + 8192, &tmA, &full[s], m0 + 64, k0, zz);
+            }
+            if (!B_MN) {
+              tma_load_3d(b_dst, &tmB, &full[s], k0, n0, zz);
+            } else {
+#pragma unroll
+              for (int c = 0; c < BN / 64; ++c) tma_load_3d(b_dst + c * 8192, &tmB, &full[s], n0 + c * 64, k0, zz);
+            }
+            if (++s == STAGES) { s = 0; ph ^= 1; }
+          }
+        }
+      }
+    } else {
+      const int tid = threadIdx.x;  // 0..127
+      for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        int64_t z; int mt, nt;
+        tile_coords(t, tiles_m, tiles_n, group_m, z, mt, nt);
+        const int64_t m0 = static_cast<int64_t>(mt) * HG_BM, n0 = static_cast<int64_t>(nt) * BN;
+        const __half* A = static_cast<const __half*>(p.a) + inst_off(p.a_off, p.stride_a, p.a_offs, z);
+        const __half* B = static_cast<const __half*>(p.b) + inst_off(p.b_off, p.stride_b, p.b_offs, z);
+        const int m_left = static_cast<int>(min64(HG_BM, p.m - m0));
+        const int n_left = static_cast<int>(min64(BN, p.n - n0));
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int64_t k0 = static_cast<int64_t>(kb) * HG_BK;
+          const int k_left = static_cast<int>(min64(HG_BK, p.k - k0));
+          mbar_wait(&empty[s], ph ^ 1);
+          // A: K-major element (i,kk) at A[i*lda + kk]; MN-major at A[i + kk*lda]
+          const __half* a_base = A_MN ? A + k0 * p.lda + m0 : A + m0 * p.lda + k0;
+          const __half* b_base = B_MN ? B + k0 * p.ldb + n0 : B + n0 * p.ldb + k0;
+          ldg_fill_tile<HG_BM, A_MN, VEC>(sA + s * C::A_BYTES, a_base, p.lda, m_left, k_left, tid);
+          ldg_fill_tile<BN, B_MN, VEC>(sB + s * C::B_BYTES, b_base, p.ldb, n_left, k_left, tid);
+          fence_proxy_async_smem();
+          mbar_arrive(&full[s]);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == C::MMA_WARP) {
+    // ======================= MMA issuer =======================
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_f16(HG_BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + s * C::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + s * C::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < HG_BK / 16; ++kk) {
+            const uint64_t adesc = A_MN ? umma_desc_sw128(a_addr + kk * 2048, 8192, 1024)
+                                        : umma_desc_sw128(a_addr + kk * 32, 16, 1024);
+            const uint64_t bdesc = B_MN ? umma_desc_sw128(b_addr + kk * 2048, 8192, 1024)
+                                        : umma_desc_sw128(b_addr + kk * 32, 16, 1024);
+            tc_mma_f16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          tc_commit(&empty[s]);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+  } else if (warp >= C::EPI_WARP0) {
+    // ======================= epilogue =======================
+    const int quad = warp & 3;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      int64_t z; int mt, nt;
+      tile_coords(t, tiles_m, tiles_n, group_m, z, mt, nt);
+      const int64_t m0 = static_cast<int64_t>(mt) * HG_BM, n0 = static_cast<int64_t>(nt) * BN;
+      Epi epi;
+      epi.alpha = inst_alpha(p, z);
+      epi.beta = inst_beta(p, z);
+      epi.skip_ab = (epi.alpha == 0.0f);
+      const int64_t row = m0 + quad * 32 + lane;
+      const bool row_ok = row < p.m;
+      __half* Cz = static_cast<__half*>(p.c) + inst_off(p.c_off, p.stride_c, p.c_offs, z);
+      const int n_left = static_cast<int>(min64(BN, p.n - n0));
+
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(acc * BN);
+#pragma unroll 1
+      for (int cb = 0; cb < BN / 32; ++cb) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_row + cb * 32, v);
+        tmem_ld_wait();
+        if (row_ok) {
+          __half* cp = Cz + (n0 + cb * 32) * p.ldc + row;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (cb * 32 + j < n_left) {
+              const float cv = epi.reads_c() ? __half2float(cp[j * p.ldc]) : 0.0f;
+              cp[j * p.ldc] = __float2half_rn(epi.apply(__uint_as_float(v[j]), cv));
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == C::ALLOC_WARP) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+// alpha == 0 / k == 0 for H (level3.py:125-132): C = beta == 0 ? 0 : RNE(beta*C)
+__global__ void hscale_kernel(Problem p) {
+  const int64_t total = p.m * p.n;
+  for (int64_t z = 0; z < p.batch; ++z) {
+    const float beta = inst_beta(p, z);
+    __half* Cz = static_cast<__half*>(p.c) + inst_off(p.c_off, p.stride_c, p.c_offs, z);
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      const int64_t i = e % p.m, j = e / p.m;
+      __half* cp = Cz + i + j * p.ldc;
+      *cp = (beta == 0.0f) ? __float2half_rn(0.0f) : __float2half_rn(__fmul_rn(beta, __half2float(*cp)));
+    }
+  }
+}
+
+}  // namespace tb

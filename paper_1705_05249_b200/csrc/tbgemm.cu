@@ -1,0 +1,403 @@
+// tbgemm.cu — C-ABI entry points (include/tbgemm.h) and kernel dispatch.
+//
+// Host-side responsibilities (all argument *validation* happened in the
+// Python routine layer, mirroring pkg/src/tunedblas/routines/level3.py:94-133
+// and extras.py:188-348):
+//   1. canonicalise layout/trans into one column-major problem (row-major C
+//      is C^T col-major: swap A<->B and m<->n — common.py:1-7, level3.py:41-45);
+//   2. map the 14 reference GemmParams (params.py:120-146) onto the nearest
+//      sm_100a instantiation;
+//   3. pick the producer (TMA when 16-byte alignment allows, LDG otherwise);
+//   4. build TMA tensor maps (cuTensorMapEncodeTiled via the runtime's
+//      driver entry point — no link-time libcuda dependency);
+//   5. launch on the caller's stream and record a tb_launch_record.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "hgemm_tc.cuh"
+#include "sgemm_simt.cuh"
+#include "tbgemm.h"
+
+using namespace tb;
+
+namespace {
+
+thread_local tb_launch_record g_last{};
+thread_local char g_last_err[256] = "";
+
+void set_err(const char* what, cudaError_t e) {
+  snprintf(g_last_err, sizeof(g_last_err), "%s: %s", what, cudaGetErrorString(e));
+}
+
+void record(const char* name, dim3 grid, dim3 block, int cluster, int smem, int64_t tiles) {
+  memset(&g_last, 0, sizeof(g_last));
+  snprintf(g_last.kernel, sizeof(g_last.kernel), "%s", name);
+  g_last.grid[0] = grid.x; g_last.grid[1] = grid.y; g_last.grid[2] = grid.z;
+  g_last.block[0] = block.x; g_last.block[1] = block.y; g_last.block[2] = block.z;
+  g_last.cluster[0] = cluster; g_last.cluster[1] = 1; g_last.cluster[2] = 1;
+  g_last.smem_bytes = smem;
+  g_last.launches = 1;
+  g_last.tiles = tiles;
+}
+
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (dev < 0 || dev >= 64) return 0;
+  if (cached[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    cached[dev] = v;
+  }
+  return cached[dev];
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_err(what, e);
+    return TB_ERR_CUDA;
+  }
+  return TB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Driver entry point for tensor maps
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) {
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    }
+  });
+  return fn;
+}
+
+// 3-D FP16 tensor map: dims {contig, other, batch}, box {box0, box1, 1}, SW128.
+int make_map(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t batch, uint64_t ld,
+             uint64_t stride, uint32_t box0, uint32_t box1) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) {
+    snprintf(g_last_err, sizeof(g_last_err), "cuTensorMapEncodeTiled entry point unavailable");
+    return TB_ERR_DRIVER;
+  }
+  cuuint64_t dims[3] = {d0, d1, batch};
+  uint64_t zstride = stride * 2;
+  if (batch <= 1) zstride = ((ld * d1 * 2) + 15) / 16 * 16;
+  cuuint64_t strides[2] = {ld * 2, zstride};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(g_last_err, sizeof(g_last_err), "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+    return TB_ERR_DRIVER;
+  }
+  return TB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Canonicalisation
+// ---------------------------------------------------------------------------
+struct Call {
+  int prec, layout, ta, tbt;
+  int64_t m, n, k;
+  Problem p;
+  int offs_aligned;  // generic batched: host-asserted offset alignment
+  const tb_gemm_params* params;
+  int flags;
+  cudaStream_t stream;
+};
+
+void canonicalize(Call& c) {
+  Problem& p = c.p;
+  int ta = c.ta, tbt = c.tbt;
+  if (c.layout == TB_ROW_MAJOR) {
+    // C_row (m x n) == C^T col-major (n x m) = op(B)^T op(A)^T
+    std::swap(p.a, p.b);
+    std::swap(p.lda, p.ldb);
+    std::swap(p.a_off, p.b_off);
+    std::swap(p.stride_a, p.stride_b);
+    std::swap(p.a_offs, p.b_offs);
+    std::swap(ta, tbt);
+    std::swap(c.m, c.n);
+  }
+  p.m = c.m;
+  p.n = c.n;
+  p.k = c.k;
+  p.a_kcontig = (ta != TB_NO_TRANS) ? 1 : 0;
+  p.b_ncontig = (tbt != TB_NO_TRANS) ? 1 : 0;
+}
+
+bool aligned_elems(const void* base, int64_t off, int64_t elem, int64_t vec_bytes) {
+  return ((reinterpret_cast<uintptr_t>(base) + off * elem) % vec_bytes) == 0;
+}
+
+// ---------------------------------------------------------------------------
+// SGEMM dispatch
+// ---------------------------------------------------------------------------
+template <int BM, int BN, int BK, int TM, int TN, bool VEC, int MINB>
+int launch_simt(const Call& c, const char* tag) {
+  const Problem& p = c.p;
+  const int tiles_m = static_cast<int>((p.m + BM - 1) / BM);
+  const int tiles_n = static_cast<int>((p.n + BN - 1) / BN);
+  const int64_t blocks = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
+  if (blocks > 0x7fffffffLL) return TB_ERR_INVALID;
+  const int group_m = 8;
+  dim3 grid(static_cast<unsigned>(blocks)), block(SimtShape<BM, BN, BK, TM, TN>::NT);
+  const int sel = (p.a_kcontig ? 2 : 0) | (p.b_ncontig ? 1 : 0);
+  switch (sel) {
+    case 0: sgemm_simt_kernel<BM, BN, BK, TM, TN, false, false, VEC, MINB><<<grid, block, 0, c.stream>>>(p, tiles_m, tiles_n, group_m); break;
+    case 1: sgemm_simt_kernel<BM, BN, BK, TM, TN, false, true, VEC, MINB><<<grid, block, 0, c.stream>>>(p, tiles_m, tiles_n, group_m); break;
+    case 2: sgemm_simt_kernel<BM, BN, BK, TM, TN, true, false, VEC, MINB><<<grid, block, 0, c.stream>>>(p, tiles_m, tiles_n, group_m); break;
+    default: sgemm_simt_kernel<BM, BN, BK, TM, TN, true, true, VEC, MINB><<<grid, block, 0, c.stream>>>(p, tiles_m, tiles_n, group_m); break;
+  }
+  char name[64];
+  static const char* lay[4] = {"mk", "mn", "kk", "kn"};  // A major x B major
+  snprintf(name, sizeof(name), "sgemm_simt_%dx%dx%d_%s_%s", BM, BN, BK, VEC ? "vec" : "gen", lay[sel]);
+  (void)tag;
+  record(name, grid, block, 1, 0, blocks);
+  return check_launch("sgemm_simt launch");
+}
+
+int dispatch_sgemm(const Call& c) {
+  const Problem& p = c.p;
+  if (c.flags & TB_FLAG_TF32) {
+    snprintf(g_last_err, sizeof(g_last_err), "TF32 SGEMM variant not built in this version");
+    return TB_ERR_UNSUPPORTED;
+  }
+  // 16-byte vector loads need every operand element base and ld to be
+  // multiples of 4 floats.
+  bool vec = (p.lda % 4 == 0) && (p.ldb % 4 == 0) && aligned_elems(p.a, 0, 4, 16) && aligned_elems(p.b, 0, 4, 16);
+  if (p.a_offs || p.b_offs) {
+    vec = vec && c.offs_aligned;
+  } else {
+    vec = vec && (p.a_off % 4 == 0) && (p.b_off % 4 == 0);
+    if (p.batch > 1) vec = vec && (p.stride_a % 4 == 0) && (p.stride_b % 4 == 0);
+  }
+  if (c.flags & TB_FLAG_SIMT_GENERAL) vec = false;
+  if (!vec) return launch_simt<64, 64, 16, 4, 4, false, 2>(c, "general");
+
+  // Parameter mapping: MWG/NWG choose the CTA tile.  Every
+  // instantiation yields bitwise-identical results (sequential-k chain).
+  int mwg = 128, nwg = 128;
+  if (c.params) { mwg = c.params->MWG; nwg = c.params->NWG; }
+  const int sms = sm_count() > 0 ? sm_count() : 148;
+  const int64_t tiles128 = ((p.m + 127) / 128) * ((p.n + 127) / 128) * p.batch;
+  if (mwg >= 128 && nwg >= 128 && tiles128 >= sms) return launch_simt<128, 128, 8, 8, 8, true, 2>(c, "128");
+  if (p.m <= 32 && p.n <= 32) return launch_simt<32, 32, 32, 4, 4, true, 8>(c, "32");
+  if (mwg >= 64 || nwg >= 64 || tiles128 < sms) return launch_simt<64, 64, 16, 4, 4, true, 2>(c, "64");
+  return launch_simt<32, 32, 32, 4, 4, true, 8>(c, "32");
+}
+
+// ---------------------------------------------------------------------------
+// HGEMM dispatch
+// ---------------------------------------------------------------------------
+template <int BN, bool TMA, bool AMN, bool BMN, bool VEC>
+int launch_hg(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
+  using Cfg = HgCfg<BN, TMA>;
+  const Problem& p = c.p;
+  const int tiles_m = static_cast<int>((p.m + HG_BM - 1) / HG_BM);
+  const int tiles_n = static_cast<int>((p.n + BN - 1) / BN);
+  const int64_t total = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
+  auto kern = hgemm_tc_kernel<BN, TMA, AMN, BMN, VEC>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) {
+      set_err("cudaFuncSetAttribute", e);
+      return TB_ERR_CUDA;
+    }
+    attr_set = true;
+  }
+  const int sms = sm_count() > 0 ? sm_count() : 148;
+  const int64_t g = total < sms ? total : sms;
+  dim3 grid(static_cast<unsigned>(g)), block(Cfg::THREADS);
+  const int group_m = 16;
+  kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, group_m, total);
+  char name[64];
+  snprintf(name, sizeof(name), "hgemm_tc_%s_128x%d_%c%c%s", TMA ? "tma" : "ldg", BN, AMN ? 'm' : 'k',
+           BMN ? 'n' : 'k', (!TMA && !VEC) ? "_scalar" : "");
+  record(name, grid, block, 1, Cfg::SMEM_BYTES, total);
+  return check_launch("hgemm_tc launch");
+}
+
+template <int BN, bool TMA, bool VEC>
+int launch_hg_layout(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
+  const bool amn = !c.p.a_kcontig, bmn = c.p.b_ncontig;
+  if (!amn && !bmn) return launch_hg<BN, TMA, false, false, VEC>(c, ta, tbm);
+  if (!amn && bmn) return launch_hg<BN, TMA, false, true, VEC>(c, ta, tbm);
+  if (amn && !bmn) return launch_hg<BN, TMA, true, false, VEC>(c, ta, tbm);
+  return launch_hg<BN, TMA, true, true, VEC>(c, ta, tbm);
+}
+
+template <int BN>
+int dispatch_hgemm_bn(const Call& c) {
+  const Problem& p = c.p;
+  const bool amn = !p.a_kcontig, bmn = p.b_ncontig;
+  // 16-byte alignment of every operand row start (TMA and LDG.128).
+  bool al = (p.lda % 8 == 0) && (p.ldb % 8 == 0) && aligned_elems(p.a, 0, 2, 16) && aligned_elems(p.b, 0, 2, 16);
+  bool generic = (p.a_offs != nullptr) || (p.b_offs != nullptr);
+  if (generic) {
+    al = al && c.offs_aligned;
+  } else {
+    al = al && (p.a_off % 8 == 0) && (p.b_off % 8 == 0);
+    if (p.batch > 1) al = al && (p.stride_a % 8 == 0) && (p.stride_b % 8 == 0);
+  }
+  const bool big = p.m < (1LL << 31) && p.n < (1LL << 31) && p.k < (1LL << 31) && p.batch < (1LL << 31);
+  CUtensorMap ta, tbm;
+  memset(&ta, 0, sizeof(ta));
+  memset(&tbm, 0, sizeof(tbm));
+  if (al && !generic && big && !(c.flags & TB_FLAG_NO_TMA)) {
+    const __half* A = static_cast<const __half*>(p.a) + p.a_off;
+    const __half* B = static_cast<const __half*>(p.b) + p.b_off;
+    int rc;
+    if (!amn) rc = make_map(&ta, A, p.k, p.m, p.batch, p.lda, p.stride_a, 64, 128);
+    else rc = make_map(&ta, A, p.m, p.k, p.batch, p.lda, p.stride_a, 64, 64);
+    if (rc != TB_OK) return rc;
+    if (!bmn) rc = make_map(&tbm, B, p.k, p.n, p.batch, p.ldb, p.stride_b, 64, BN);
+    else rc = make_map(&tbm, B, p.n, p.k, p.batch, p.ldb, p.stride_b, 64, 64);
+    if (rc != TB_OK) return rc;
+    return launch_hg_layout<BN, true, true>(c, ta, tbm);
+  }
+  if (al) return launch_hg_layout<BN, false, true>(c, ta, tbm);
+  return launch_hg_layout<BN, false, false>(c, ta, tbm);
+}
+
+int dispatch_hgemm(const Call& c) {
+  if (c.flags & TB_FLAG_TF32) {
+    snprintf(g_last_err, sizeof(g_last_err), "TF32 flag applies to SGEMM only");
+    return TB_ERR_UNSUPPORTED;
+  }
+  // Parameter mapping: NWG picks the UMMA N extent.  Pure function of the
+  // parameters (never of batch) so single and batched calls of one shape use
+  // the same MMA sequence (bitwise batched == looped).
+  int nwg = 128;
+  if (c.params) nwg = c.params->NWG;
+  if (nwg >= 128) return dispatch_hgemm_bn<256>(c);
+  if (nwg >= 64) return dispatch_hgemm_bn<128>(c);
+  return dispatch_hgemm_bn<64>(c);
+}
+
+int launch_hscale(const Call& c) {
+  dim3 block(256);
+  const int64_t total = c.p.m * c.p.n;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  if (blocks < 1) blocks = 1;
+  dim3 grid(static_cast<unsigned>(blocks));
+  hscale_kernel<<<grid, block, 0, c.stream>>>(c.p);
+  record("hscale", grid, block, 1, 0, c.p.batch);
+  return check_launch("hscale launch");
+}
+
+int run(Call& c) {
+  memset(&g_last, 0, sizeof(g_last));
+  if (c.m < 0 || c.n < 0 || c.k < 0 || c.p.batch < 1) return TB_ERR_INVALID;
+  if (c.prec != TB_PREC_H && c.prec != TB_PREC_S) return TB_ERR_INVALID;
+  if (c.m == 0 || c.n == 0) return TB_OK;
+  canonicalize(c);
+  if (c.prec == TB_PREC_S) return dispatch_sgemm(c);
+  // H: alpha == 0 everywhere or k == 0 never touches the tensor cores.
+  if (c.k == 0 || (c.p.alphas == nullptr && c.p.alpha == 0.0f)) return launch_hscale(c);
+  return dispatch_hgemm(c);
+}
+
+Call make_call(int prec, int layout, int ta, int tbt, int64_t m, int64_t n, int64_t k, const void* a, int64_t lda,
+               const void* b, int64_t ldb, void* cc, int64_t ldc, const tb_gemm_params* params, int flags,
+               void* stream) {
+  Call c;
+  memset(&c, 0, sizeof(c));
+  c.prec = prec; c.layout = layout; c.ta = ta; c.tbt = tbt;
+  c.m = m; c.n = n; c.k = k;
+  c.p.a = a; c.p.lda = lda;
+  c.p.b = b; c.p.ldb = ldb;
+  c.p.c = cc; c.p.ldc = ldc;
+  c.params = params;
+  c.flags = flags;
+  c.stream = static_cast<cudaStream_t>(stream);
+  c.p.batch = 1;
+  return c;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tb_gemm(int prec, int layout, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, float alpha,
+            const void* a, int64_t a_off, int64_t lda, const void* b, int64_t b_off, int64_t ldb, float beta,
+            void* c, int64_t c_off, int64_t ldc, const tb_gemm_params* params, int flags, void* stream) {
+  Call call = make_call(prec, layout, trans_a, trans_b, m, n, k, a, lda, b, ldb, c, ldc, params, flags, stream);
+  call.p.a_off = a_off; call.p.b_off = b_off; call.p.c_off = c_off;
+  call.p.alpha = alpha; call.p.beta = beta;
+  return run(call);
+}
+
+int tb_gemm_strided_batched(int prec, int layout, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
+                            float alpha, const void* a, int64_t a_off, int64_t lda, int64_t stride_a, const void* b,
+                            int64_t b_off, int64_t ldb, int64_t stride_b, float beta, void* c, int64_t c_off,
+                            int64_t ldc, int64_t stride_c, int64_t batch, const tb_gemm_params* params, int flags,
+                            void* stream) {
+  Call call = make_call(prec, layout, trans_a, trans_b, m, n, k, a, lda, b, ldb, c, ldc, params, flags, stream);
+  call.p.a_off = a_off; call.p.b_off = b_off; call.p.c_off = c_off;
+  call.p.stride_a = stride_a; call.p.stride_b = stride_b; call.p.stride_c = stride_c;
+  call.p.alpha = alpha; call.p.beta = beta;
+  call.p.batch = batch;
+  return run(call);
+}
+
+int tb_gemm_batched(int prec, int layout, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
+                    const float* alphas, const void* a, const int64_t* a_offs, int64_t lda, const void* b,
+                    const int64_t* b_offs, int64_t ldb, const float* betas, void* c, const int64_t* c_offs,
+                    int64_t ldc, int64_t batch, int offs_aligned, const tb_gemm_params* params, int flags,
+                    void* stream) {
+  if (!alphas || !betas || !a_offs || !b_offs || !c_offs) return TB_ERR_INVALID;
+  Call call = make_call(prec, layout, trans_a, trans_b, m, n, k, a, lda, b, ldb, c, ldc, params, flags, stream);
+  call.p.a_offs = a_offs; call.p.b_offs = b_offs; call.p.c_offs = c_offs;
+  call.p.alphas = alphas; call.p.betas = betas;
+  call.p.alpha = 1.0f; call.p.beta = 0.0f;
+  call.p.batch = batch;
+  call.offs_aligned = offs_aligned;
+  return run(call);
+}
+
+int tb_last_launch(tb_launch_record* out) {
+  if (!out) return TB_ERR_INVALID;
+  *out = g_last;
+  return TB_OK;
+}
+
+const char* tb_status_str(int status) {
+  switch (status) {
+    case TB_OK: return "ok";
+    case TB_ERR_INVALID: return "invalid argument";
+    case TB_ERR_CUDA: return "CUDA error";
+    case TB_ERR_UNSUPPORTED: return "unsupported";
+    case TB_ERR_DRIVER: return "driver entry point / tensor map error";
+    default: return "unknown status";
+  }
+}
+
+const char* tb_last_error(void) { return g_last_err; }
+
+int tb_abi_version(void) { return TBGEMM_ABI_VERSION; }
+
+int tb_device_sm_count(void) { return sm_count(); }
+
+}  // extern "C"

@@ -1,0 +1,166 @@
+"""ctypes binding of libtbgemm.so — the C-ABI declared in include/tbgemm.h.
+
+The native library is the ONLY compute path: there is no CPU fallback.  If
+the shared object is missing or fails to load, every routine call raises
+:class:`NativeLibraryError` (loudly), mirroring how the reference's
+``run_kernel`` (pkg/src/tunedblas/kernels/compute.py:116-130) is the single
+place arithmetic happens.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+from ..errors import TunedBlasError
+
+__all__ = [
+    "NativeLibraryError",
+    "TbGemmParams",
+    "TbLaunchRecord",
+    "lib",
+    "library_path",
+    "EXPORTED_SYMBOLS",
+    "PREC_H",
+    "PREC_S",
+    "COL_MAJOR",
+    "ROW_MAJOR",
+    "FLAG_TF32",
+    "FLAG_NO_TMA",
+    "FLAG_SIMT_GENERAL",
+]
+
+PREC_H, PREC_S = 0, 1
+COL_MAJOR, ROW_MAJOR = 0, 1
+NO_TRANS, TRANS, CONJ_TRANS = 0, 1, 2
+FLAG_TF32, FLAG_NO_TMA, FLAG_SIMT_GENERAL = 1, 2, 4
+TB_OK = 0
+
+#: Every symbol include/tbgemm.h declares (checked by tests/test_native_abi.py).
+EXPORTED_SYMBOLS = (
+    "tb_gemm",
+    "tb_gemm_strided_batched",
+    "tb_gemm_batched",
+    "tb_last_launch",
+    "tb_status_str",
+    "tb_last_error",
+    "tb_abi_version",
+    "tb_device_sm_count",
+)
+
+
+class NativeLibraryError(TunedBlasError, RuntimeError):
+    """The CUDA library could not be loaded or a kernel launch failed."""
+
+
+_PARAM_NAMES = ("MWG", "NWG", "KWG", "MDIMC", "NDIMC", "MDIMA", "NDIMB",
+                "KWI", "VWM", "VWN", "STRM", "STRN", "SA", "SB")
+
+
+class TbGemmParams(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_int32) for name in _PARAM_NAMES]
+
+    @classmethod
+    def from_dict(cls, values: dict) -> "TbGemmParams":
+        return cls(*(int(values[name]) for name in _PARAM_NAMES))
+
+
+class TbLaunchRecord(ctypes.Structure):
+    _fields_ = [
+        ("kernel", ctypes.c_char * 64),
+        ("grid", ctypes.c_int64 * 3),
+        ("block", ctypes.c_int32 * 3),
+        ("cluster", ctypes.c_int32 * 3),
+        ("smem_bytes", ctypes.c_int32),
+        ("launches", ctypes.c_int32),
+        ("tiles", ctypes.c_int64),
+    ]
+
+    def to_dict(self) -> dict:
+        return {
+            "kernel": self.kernel.decode(),
+            "grid": tuple(self.grid),
+            "block": tuple(self.block),
+            "cluster": tuple(self.cluster),
+            "smem_bytes": int(self.smem_bytes),
+            "launches": int(self.launches),
+            "tiles": int(self.tiles),
+        }
+
+
+def library_path() -> Path:
+    override = os.environ.get("TBGEMM_LIB")
+    if override:
+        return Path(override)
+    return Path(__file__).resolve().parent.parent / "_lib" / "libtbgemm.so"
+
+
+_lock = threading.Lock()
+_lib = None
+
+_i32, _i64, _f32, _vp = ctypes.c_int, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p
+_P = ctypes.POINTER
+
+
+def _declare(so) -> None:
+    so.tb_gemm.restype = _i32
+    so.tb_gemm.argtypes = [_i32, _i32, _i32, _i32, _i64, _i64, _i64, _f32,
+                           _vp, _i64, _i64, _vp, _i64, _i64, _f32,
+                           _vp, _i64, _i64, _P(TbGemmParams), _i32, _vp]
+    so.tb_gemm_strided_batched.restype = _i32
+    so.tb_gemm_strided_batched.argtypes = [
+        _i32, _i32, _i32, _i32, _i64, _i64, _i64, _f32,
+        _vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _f32,
+        _vp, _i64, _i64, _i64, _i64, _P(TbGemmParams), _i32, _vp]
+    so.tb_gemm_batched.restype = _i32
+    so.tb_gemm_batched.argtypes = [
+        _i32, _i32, _i32, _i32, _i64, _i64, _i64, _vp,
+        _vp, _vp, _i64, _vp, _vp, _i64, _vp,
+        _vp, _vp, _i64, _i64, _i32, _P(TbGemmParams), _i32, _vp]
+    so.tb_last_launch.restype = _i32
+    so.tb_last_launch.argtypes = [_P(TbLaunchRecord)]
+    so.tb_status_str.restype = ctypes.c_char_p
+    so.tb_status_str.argtypes = [_i32]
+    so.tb_last_error.restype = ctypes.c_char_p
+    so.tb_last_error.argtypes = []
+    so.tb_abi_version.restype = _i32
+    so.tb_abi_version.argtypes = []
+    so.tb_device_sm_count.restype = _i32
+    so.tb_device_sm_count.argtypes = []
+
+
+def lib():
+    """The loaded library (raises NativeLibraryError when unavailable)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            path = library_path()
+            if not path.exists():
+                raise NativeLibraryError(
+                    f"CUDA library {path} is missing; run __graft_entry__.build() "
+                    "(there is no CPU fallback)")
+            try:
+                so = ctypes.CDLL(str(path))
+            except OSError as exc:
+                raise NativeLibraryError(f"cannot load {path}: {exc}") from exc
+            _declare(so)
+            _lib = so
+    return _lib
+
+
+def check(status: int, what: str) -> None:
+    if status != TB_OK:
+        so = lib()
+        raise NativeLibraryError(
+            f"{what} failed: {so.tb_status_str(status).decode()} "
+            f"({so.tb_last_error().decode()})")
+
+
+def last_launch() -> dict:
+    rec = TbLaunchRecord()
+    check(lib().tb_last_launch(ctypes.byref(rec)), "tb_last_launch")
+    return rec.to_dict()
