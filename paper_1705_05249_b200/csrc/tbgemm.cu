@@ -192,18 +192,24 @@ int dispatch_sgemm(const Call& c) {
     if (p.batch > 1) vec = vec && (p.stride_a % 4 == 0) && (p.stride_b % 4 == 0);
   }
   if (c.flags & TB_FLAG_SIMT_GENERAL) vec = false;
-  if (!vec) return launch_simt<64, 64, 16, 4, 4, false, 2>(c, "general");
-
-  // Parameter mapping: MWG/NWG choose the CTA tile.  Every
-  // instantiation yields bitwise-identical results (sequential-k chain).
+  // Parameter mapping: VWM = VWN = 1 asks for scalar loads; MWG /
+  // NWG choose the CTA tile.  Every instantiation yields bitwise-identical
+  // results (sequential-k chain), so the mapping is free to follow speed.
   int mwg = 128, nwg = 128;
-  if (c.params) { mwg = c.params->MWG; nwg = c.params->NWG; }
+  if (c.params) {
+    mwg = c.params->MWG;
+    nwg = c.params->NWG;
+    if (c.params->VWM == 1 && c.params->VWN == 1) vec = false;
+  }
+  if (!vec) return launch_simt<64, 64, 16, 4, 4, false, 2>(c, "general");
   const int sms = sm_count() > 0 ? sm_count() : 148;
   const int64_t tiles128 = ((p.m + 127) / 128) * ((p.n + 127) / 128) * p.batch;
-  if (mwg >= 128 && nwg >= 128 && tiles128 >= sms) return launch_simt<128, 128, 8, 8, 8, true, 2>(c, "128");
   if (p.m <= 32 && p.n <= 32) return launch_simt<32, 32, 32, 4, 4, true, 8>(c, "32");
-  if (mwg >= 64 || nwg >= 64 || tiles128 < sms) return launch_simt<64, 64, 16, 4, 4, true, 2>(c, "64");
-  return launch_simt<32, 32, 32, 4, 4, true, 8>(c, "32");
+  if (mwg >= 128 && nwg >= 128 && tiles128 >= sms) return launch_simt<128, 128, 8, 8, 8, true, 2>(c, "128");
+  if (mwg >= 128 && nwg < 128 && tiles128 * 2 >= sms) return launch_simt<128, 64, 16, 8, 4, true, 2>(c, "128x64");
+  if (mwg < 128 && nwg >= 128 && tiles128 * 2 >= sms) return launch_simt<64, 128, 16, 4, 8, true, 2>(c, "64x128");
+  if (mwg <= 32 && nwg <= 32) return launch_simt<32, 32, 32, 4, 4, true, 8>(c, "32");
+  return launch_simt<64, 64, 16, 4, 4, true, 2>(c, "64");
 }
 
 // ---------------------------------------------------------------------------

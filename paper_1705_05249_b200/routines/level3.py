@@ -1,0 +1,88 @@
+"""Level-3 GEMM: the public ``gemm`` routine (level3.py:94-149 of the
+reference) over the sm_100a kernels.
+
+Validation, defaults, early-outs and error text follow the reference step by
+step (SURVEY §9 "Order of checks in gemm").  The reference then materialised
+op(A) and op(B)^T, padded them to tile multiples and unpadded the result
+(level3.py:134-147, 48-91); here the unpadded operands go straight to
+libtbgemm.so, which reads them in place (TMA tensor maps / predicated loads)
+and fuses the single rounding into its epilogue.
+"""
+
+from __future__ import annotations
+
+from ..core import Buffer, Context, Layout, Precision, Transpose
+from ..errors import UsageError
+from ..kernels import native
+from ..kernels.dispatch import gemm_native, prec_code
+from ..kernels.engine import pre_launch, record_launch, reference_grid
+from .common import check_logical, check_precision, default_ld, get_store, scalar, stored_dims
+
+__all__ = ["gemm", "route_family", "route_flags"]
+
+
+def route_family(m: int, n: int, k: int, threshold: int, kernel: str | None) -> str:
+    """"direct" below the store's threshold (level3.py:57-59), else "indirect"."""
+    if kernel is None:
+        kernel = "direct" if max(m, n, k) < threshold else "indirect"
+    return kernel
+
+
+def route_flags(kernel_forced: str | None) -> int:
+    """An explicit ``kernel="direct"`` selects the bounds-checked producers
+    (SIMT general kernel / tcgen05 with LDG producer); they are bitwise
+    identical to the tiled ones, so default routing only sets the family."""
+    if kernel_forced == "direct":
+        return native.FLAG_SIMT_GENERAL | native.FLAG_NO_TMA
+    return 0
+
+
+def gemm(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Transpose,
+         m: int, n: int, k: int, alpha, a: Buffer, b: Buffer, beta, c: Buffer, *,
+         a_offset: int = 0, lda: int | None = None,
+         b_offset: int = 0, ldb: int | None = None,
+         c_offset: int = 0, ldc: int | None = None,
+         kernel: str | None = None) -> None:
+    """C = alpha * op(A) op(B) + beta * C on the GPU (asynchronous on the
+    context's stream; read results with ``buffer_read`` / ``Buffer.data``).
+
+    ``kernel`` forces the 'direct' or 'indirect' route (reference testing
+    knob, level3.py:99,110-111).
+    """
+    precision = a.precision
+    check_precision(ctx, precision, a, b, c)
+    if m < 0 or n < 0 or k < 0:
+        raise UsageError("gemm dimensions must be >= 0")
+    if kernel not in (None, "direct", "indirect"):
+        raise UsageError("kernel must be None, 'direct' or 'indirect'")
+    prec_code(precision)  # H / S only on this path
+    if m == 0 or n == 0:
+        return
+    a_rows, a_cols = stored_dims(trans_a, m, k)
+    b_rows, b_cols = stored_dims(trans_b, k, n)
+    lda = lda if lda is not None else default_ld(layout, a_rows, a_cols)
+    ldb = ldb if ldb is not None else default_ld(layout, b_rows, b_cols)
+    ldc = ldc if ldc is not None else (m if layout is Layout.COL_MAJOR else n)
+    check_logical(a, a_offset, a_rows, a_cols, lda, layout)
+    check_logical(b, b_offset, b_rows, b_cols, ldb, layout)
+    check_logical(c, c_offset, m, n, ldc, layout)
+
+    alpha = scalar(alpha, precision)
+    beta = scalar(beta, precision)
+    store = get_store(ctx)
+    if k == 0 or alpha == 0:
+        # Only the beta scaling remains; A and B are never read
+        # (level3.py:125-132).  No LaunchRecord, as in the reference.
+        gemm_native(ctx, precision, layout, trans_a, trans_b, m, n, k, alpha,
+                    a, a_offset, lda, b, b_offset, ldb, beta, c, c_offset, ldc, None)
+        return
+
+    cfg, _ = store.resolve("gemm", precision, ctx.device, (m, n, k))
+    route = route_family(m, n, k, store.direct_threshold, kernel)
+    family = "gemm_direct" if route == "direct" else "gemm"
+    grid = reference_grid(family, m, n, cfg)
+    pre_launch(ctx, family, cfg, grid, precision)
+    launched = gemm_native(ctx, precision, layout, trans_a, trans_b, m, n, k, alpha,
+                           a, a_offset, lda, b, b_offset, ldb, beta, c, c_offset, ldc,
+                           cfg, route_flags(kernel))
+    record_launch(ctx, family, cfg, grid, launched)
