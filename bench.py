@@ -1,0 +1,485 @@
+#!/usr/bin/env python3
+"""Driver benchmark: GEMM GFLOPS of the B200-native hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload hgemm|sgemm|batched_h32|batched_s32|batched_h64|batched_s64]
+                    [--no-extra] [--no-cpu-baseline]
+
+A "step" is one call of the hot path on one batch of synthetic input:
+* hgemm (default, the headline): C = A·B, 8192^3, FP16 storage / FP32
+  accumulate, row-major NN, alpha=1, beta=0 (BASELINE configs[1], largest
+  square size of the sweep);
+* sgemm: the same shape in FP32 (FFMA);
+* batched_*: gemm_strided_batched, 16384 instances of 32^3 / 64^3 (configs[3]).
+
+value   = whole-job GFLOPS with inputs resident in HBM, CUDA-event timed per
+          step on the launching stream (max over ranks), L2 flushed between
+          steps (a 256 MiB write) so no step reads a warm L2.
+e2e     = the same metric through the public API with HOST buffers: pinned
+          host → device copy of A and B, the routine, device → host copy of C,
+          all inside the timed region.
+N > 1   = weak scaling: rank r computes its own 8192-column block of an
+          8192 x (8192·N) x 8192 GEMM (column-sharded C, no collective) or its
+          own 16384-instance block of the batch.
+--impl reference times the reference's CPU implementation of the path (the
+oracle port of tunedblas' tiled algorithm, oracle/gemm_oracle.py) on the
+host cores, each step a bounded row-block sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "GEMM GFLOPS (SGEMM/HGEMM, batched) and % of B200 peak at 1/2/4/8 GPUs"
+FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+FFMA_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # derived FP32 FFMA peak at sm_max_mhz
+
+
+def load_peaks():
+    path = ROOT / "MEASURED_PEAKS.json"
+    if path.exists():
+        with open(path) as fh:
+            doc = json.load(fh)
+        return doc, "measured"
+    return dict(FALLBACK), "fallback"
+
+
+WORKLOADS = {
+    "hgemm": dict(kind="gemm", prec="H", m=8192, n=8192, k=8192, batch=1),
+    "sgemm": dict(kind="gemm", prec="S", m=8192, n=8192, k=8192, batch=1),
+    "batched_h32": dict(kind="batched", prec="H", m=32, n=32, k=32, batch=16384),
+    "batched_s32": dict(kind="batched", prec="S", m=32, n=32, k=32, batch=16384),
+    "batched_h64": dict(kind="batched", prec="H", m=64, n=64, k=64, batch=16384),
+    "batched_s64": dict(kind="batched", prec="S", m=64, n=64, k=64, batch=16384),
+}
+
+
+def describe(w: dict) -> str:
+    p = "HGEMM FP16 (FP32 accumulate)" if w["prec"] == "H" else "SGEMM FP32 (FFMA)"
+    if w["kind"] == "gemm":
+        return f"{p} {w['m']}x{w['n']}x{w['k']} row-major NN alpha=1 beta=0"
+    return f"{p} strided batched {w['batch']} x {w['m']}^3 row-major NN alpha=1 beta=0"
+
+
+def flops(w: dict) -> float:
+    return 2.0 * w["m"] * w["n"] * w["k"] * w["batch"]
+
+
+def alg_bytes(w: dict) -> float:
+    es = 2 if w["prec"] == "H" else 4
+    return (w["m"] * w["k"] + w["k"] * w["n"] + w["m"] * w["n"]) * es * w["batch"]
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (pynvml poller)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self.ok = False
+        self.period = period_s
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001
+            self.ok = False
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        s = sorted(self.samples)
+        return {"sm_mhz": float(s[len(s) // 2]), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(s)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def make_operands(tb, ctx, w, rank, world, torch):
+    prec = tb.Precision.H if w["prec"] == "H" else tb.Precision.S
+    dt = prec.torch_dtype
+    dev = ctx.torch_device
+    g = torch.Generator(device=dev).manual_seed(12345 + rank)
+    if w["kind"] == "gemm":
+        m, n, k = w["m"], w["n"], w["k"]
+        # rank's column block of an m x (n*world) x k GEMM: A (m x k) replicated,
+        # B block (k x n) and C block (m x n) local — row-major packed.
+        na, nb, nc = m * k, k * n, m * n
+    else:
+        e = w["m"] * w["k"]
+        na = nb = nc = e * w["batch"]
+    at = (torch.rand(na, device=dev, generator=g) * 2 - 1).to(dt)
+    bt = (torch.rand(nb, device=dev, generator=g) * 2 - 1).to(dt)
+    ct = torch.zeros(nc, device=dev, dtype=dt)
+    return prec, tb.buffer_from_tensor(ctx, prec, at), tb.buffer_from_tensor(ctx, prec, bt), \
+        tb.buffer_from_tensor(ctx, prec, ct)
+
+
+def step_fn(tb, ctx, w, prec, a, b, c):
+    L, T = tb.Layout.ROW_MAJOR, tb.Transpose.NO
+    if w["kind"] == "gemm":
+        m, n, k = w["m"], w["n"], w["k"]
+        return lambda: tb.gemm(ctx, L, T, T, m, n, k, 1.0, a, b, 0.0, c)
+    m, e, bt = w["m"], w["m"] * w["m"], w["batch"]
+    return lambda: tb.gemm_strided_batched(ctx, L, T, T, m, m, m, 1.0, a, e, b, e, 0.0, c, e, bt)
+
+
+def device_time(fn, steps, warmup, stream, torch, flush):
+    """Per-step CUDA-event times (s) on `stream`, L2 flushed before each step."""
+    for _ in range(warmup):
+        flush()
+        fn()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    torch.cuda.synchronize()
+    for e0, e1 in evs:
+        flush()
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    return [e0.elapsed_time(e1) / 1e3 for e0, e1 in evs]
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1705_05249_b200 as tb
+    from paper_1705_05249_b200.kernels import native
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    ctx = tb.context_create(tb.host_device())
+    ctx.device_index = local_rank
+    stream = torch.cuda.current_stream(dev)
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = lambda: flush_buf.fill_(1)  # noqa: E731  (256 MiB > 126 MB L2)
+    peaks, peak_src = load_peaks()
+
+    def measure(name, steps, warmup):
+        w = WORKLOADS[name]
+        prec, a, b, c = make_operands(tb, ctx, w, rank, world, torch)
+        fn = step_fn(tb, ctx, w, prec, a, b, c)
+        fn()
+        torch.cuda.synchronize()
+        kernel = ctx.last_launch.native["kernel"]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        sampler = ClockSampler(local_rank)
+        with sampler:
+            times = device_time(fn, steps, warmup, stream, torch, flush)
+        total = sum(times)
+        if world > 1:
+            t = torch.tensor([total], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total = float(t.item())
+        per_launch = total / steps
+        gflops = flops(w) * world * steps / total / 1e9
+        if w["prec"] == "H" and w["kind"] == "gemm":
+            bound = "tensor"
+            peak, unit, achieved = peaks["bf16_tflops"], "TFLOP/s", flops(w) / per_launch / 1e12
+            peak_note = f"dense FP16/BF16 tensor, burst ({peak_src}: MEASURED_PEAKS.json bf16_tflops)"
+        elif w["kind"] == "gemm":
+            bound = "ffma"
+            peak, unit, achieved = FFMA_TFLOPS, "TFLOP/s", flops(w) / per_launch / 1e12
+            peak_note = "FP32 FFMA 148 SM x 128 lanes x 2 x 1.965 GHz (derived, no measured FFMA peak)"
+        else:
+            bound = "hbm"
+            peak, unit, achieved = peaks["hbm_gbs"], "GB/s", alg_bytes(w) / per_launch / 1e9
+            peak_note = f"HBM copy bandwidth ({peak_src}: MEASURED_PEAKS.json hbm_gbs)"
+        return dict(name=name, w=w, times=times, total=total, gflops=gflops, kernel=kernel,
+                    clocks=sampler.summary(), a=a, b=b, c=c, prec=prec, fn=fn,
+                    roofline={"bound": bound, "achieved": round(achieved, 2), "peak": peak,
+                              "unit": unit, "frac": round(achieved / peak, 4),
+                              "traffic": None, "peak_source": peak_note,
+                              "kernel": kernel, "per_launch_ms": round(per_launch * 1e3, 4),
+                              "algorithmic": f"{flops(w):.4g} FLOP, {alg_bytes(w):.4g} B per launch"})
+
+    main = measure(args.workload, args.steps, args.warmup)
+    w = main["w"]
+
+    # ---- e2e: public API with host buffers, copies inside the timed region ----
+    prec, a, b, c = main["prec"], main["a"], main["b"], main["c"]
+    host_a = torch.empty(a.length, dtype=prec.torch_dtype, pin_memory=True)
+    host_b = torch.empty(b.length, dtype=prec.torch_dtype, pin_memory=True)
+    host_c = torch.empty(c.length, dtype=prec.torch_dtype, pin_memory=True)
+    host_a.copy_(a.device_tensor())
+    host_b.copy_(b.device_tensor())
+    dev_a, dev_b, dev_c = a.device_tensor(), b.device_tensor(), c.device_tensor()
+    fn = main["fn"]
+
+    def e2e_step():
+        dev_a.copy_(host_a, non_blocking=True)
+        dev_b.copy_(host_b, non_blocking=True)
+        fn()
+        host_c.copy_(dev_c, non_blocking=True)
+
+    e2e_steps = max(3, min(args.steps, 20))
+    if world > 1:
+        dist.barrier()
+    e2e_times = device_time(e2e_step, e2e_steps, max(1, args.warmup), stream, torch, lambda: None)
+    e2e_total = sum(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_total], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    es = prec.elemsize
+    e2e = {"value": round(flops(w) * world * e2e_steps / e2e_total / 1e9, 2), "unit": "GFLOPS",
+           "h2d_bytes_per_step": (a.length + b.length) * es, "d2h_bytes_per_step": c.length * es,
+           "ms_per_step": round(e2e_total / e2e_steps * 1e3, 4),
+           "path": "pinned host A,B -> device; gemm (C-ABI via public API); device C -> pinned host"}
+
+    # ---- extras: the other headline configs (device-timed, this rank) ----
+    extra = {}
+    if not args.no_extra:
+        for name in WORKLOADS:
+            if name == args.workload:
+                continue
+            try:
+                r = measure(name, max(5, min(args.steps, 20)), args.warmup)
+                extra[name] = {"workload": describe(r["w"]), "value": round(r["gflops"], 1),
+                               "unit": "GFLOPS", "ms_per_step": round(r["total"] / max(1, len(r["times"])) * 1e3, 4),
+                               "roofline": r["roofline"], "clocks": r["clocks"]}
+                del r
+            except Exception as exc:  # noqa: BLE001
+                extra[name] = {"error": repr(exc)}
+            torch.cuda.empty_cache()
+
+    if rank != 0:
+        return None
+    traffic = load_traffic(main["kernel"])
+    if traffic is not None:
+        main["roofline"]["traffic"] = traffic
+    line = {
+        "metric": METRIC,
+        "value": round(main["gflops"], 2),
+        "unit": "GFLOPS",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(main["total"] / args.steps * 1e3, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f16" if w["prec"] == "H" else "f32",
+        "data": "synthetic U(-1,1) operands, seeded, resident in HBM",
+        "config": {"workload": describe(w), "m": w["m"], "n": w["n"] * (world if w["kind"] == "gemm" else 1),
+                   "k": w["k"], "batch": w["batch"] * (world if w["kind"] == "batched" else 1),
+                   "layout": "row-major", "trans": "NN", "alpha": 1.0, "beta": 0.0,
+                   "parallelism": f"column-sharded x{world}" if w["kind"] == "gemm" else f"batch-sharded x{world}",
+                   "l2": "flushed before every step (256 MiB write)"},
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+        "kernel": main["kernel"],
+        "clocks": main["clocks"],
+        "roofline": main["roofline"],
+        "frac_of_peak": main["roofline"]["frac"],
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(w, seconds_budget=args.cpu_seconds)
+    if extra:
+        line["extra"] = extra
+    return line
+
+
+def load_traffic(kernel: str):
+    """dram bytes per launch from the committed ncu capture, if one matches."""
+    path = ROOT / "profiles" / "traffic.json"
+    if not path.exists():
+        return None
+    try:
+        with open(path) as fh:
+            doc = json.load(fh)
+        return doc.get(kernel)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU: the reference's algorithm (oracle port) on the host cores
+# ---------------------------------------------------------------------------
+def cpu_sample(w: dict, rows: int | None = None):
+    """A bounded sample of the workload: a row block of the same GEMM (same
+    K and N), or a prefix of the batch.  Returns (callable, flops)."""
+    import numpy as np
+
+    from oracle import gemm_oracle as orc
+
+    dt = np.float16 if w["prec"] == "H" else np.float32
+    rng = np.random.default_rng(12345)
+    pool = orc.make_pool()
+    if w["kind"] == "gemm":
+        m = rows or 512
+        k, n = w["k"], w["n"]
+        a = rng.uniform(-1, 1, m * k).astype(dt)
+        b = rng.uniform(-1, 1, k * n).astype(dt)
+        c = np.zeros(m * n, dt)
+
+        def run():
+            orc.port_gemm(w["prec"], True, False, False, m, n, k, 1.0, a, b, 0.0, c, pool=pool)
+
+        return run, 2.0 * m * n * k, f"row block {m} x {n} x {k} of the {describe(w)}"
+    batch = rows or 256
+    e = w["m"] * w["k"]
+    a = rng.uniform(-1, 1, batch * e).astype(dt)
+    b = rng.uniform(-1, 1, batch * e).astype(dt)
+    c = np.zeros(batch * e, dt)
+
+    def run():
+        orc.port_gemm_strided_batched(w["prec"], True, False, False, w["m"], w["n"], w["k"], 1.0,
+                                      a, e, b, e, 0.0, c, e, batch)
+
+    return run, 2.0 * w["m"] * w["n"] * w["k"] * batch, \
+        f"first {batch} instances of the {describe(w)} (sequential backend, as the reference's fastest batched mode)"
+
+
+def prewarm(seconds=3.0):
+    import numpy as np
+
+    x = np.ones((512, 512), np.float32)
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        x @ x
+
+
+def cpu_baseline(w: dict, seconds_budget: float = 12.0) -> dict:
+    import numpy as np
+
+    prewarm(3.0)
+    run, fl, sample = cpu_sample(w)
+    run()
+    t0 = time.perf_counter()
+    run()
+    one = time.perf_counter() - t0
+    reps = max(1, int(seconds_budget / max(one, 1e-6)))
+    reps = min(reps, 50)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    value = fl / float(np.mean(times)) / 1e9
+    return {"value": round(value, 3), "unit": "GFLOPS", "cores": os.cpu_count(), "kind": "port",
+            "sample": sample + f"; {reps} timed runs after 1 warm-up and a 3 s pre-warm",
+            "impl": "oracle/gemm_oracle.py port_gemm (tunedblas tiled algorithm, built-in "
+                    "config MWG=NWG=64 KWG=16 KWI=8, ThreadPool of os.cpu_count() workers + OpenBLAS)"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU algorithm on the host cores."""
+    if rank != 0:
+        return None
+    import numpy as np
+
+    w = WORKLOADS[args.workload]
+    prewarm(3.0)
+    run, fl, sample = cpu_sample(w)
+    for _ in range(args.warmup):
+        run()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    value = fl / float(np.mean(times)) / 1e9
+    return {
+        "metric": METRIC, "value": round(value, 3), "unit": "GFLOPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(float(np.mean(times)) * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f16" if w["prec"] == "H" else "f32",
+        "data": "synthetic U(-1,1)", "impl": "reference",
+        "config": {"workload": describe(w), "sample": sample},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOPS", "cores": os.cpu_count(),
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "GFLOPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="hgemm")
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        line = run_ours(args, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()
