@@ -31,6 +31,7 @@ struct Problem {
   const float* alphas; const float* betas;
   int64_t batch;
   int a_kcontig, b_ncontig;
+  int dbg;  // experiment switches (0 in production)
 };
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -201,4 +202,20 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+}  // namespace tb
+
+namespace tb {
+// ---------------------------------------------------------------------------
+// cp.async (LDGSTS): 16-byte global -> shared, zero-filling past src_bytes
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gsrc, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gsrc),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 }  // namespace tb

@@ -41,13 +41,16 @@ struct HgCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                   : (2 * BN <= 256) ? 256 : 512;
+  // warps 0-7: epilogue (warp w reads TMEM lane quadrant w%4, column half
+  // w/4); then the producer warp(s); the last warp allocates TMEM and issues MMAs.
+  static constexpr int EPI_WARPS = 8;
   static constexpr int PROD_WARPS = TMA ? 1 : 4;
-  static constexpr int MMA_WARP = TMA ? 1 : 4;
-  static constexpr int ALLOC_WARP = TMA ? 2 : 5;
-  static constexpr int EPI_WARP0 = TMA ? 4 : 8;
-  static constexpr int THREADS = (EPI_WARP0 + 4) * 32;
+  static constexpr int PROD_WARP0 = EPI_WARPS;
+  static constexpr int MMA_WARP = EPI_WARPS + PROD_WARPS;
+  static constexpr int THREADS = (MMA_WARP + 1) * 32;
   static constexpr int BAR_BYTES = 1024;
-  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES;
+  static constexpr int EPI_BYTES = EPI_WARPS * 32 * 32 * 4;
+  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES + EPI_BYTES;
 };
 
 // Swizzle-128B placement of 16-byte chunk `c` (0..7) of 128-byte row `r`
@@ -113,6 +116,75 @@ __device__ __forceinline__ void ldg_fill_tile(uint8_t* smem, const __half* base,
   }
 }
 
+
+// Per-warp epilogue staging: 32 rows x 32 FP32 columns (4 KB).  Column c
+// holds row r at float index c*32 + (r ^ 4*(c%8)): conflict-free for the
+// row-per-lane writes and for the 8-rows-per-lane float4 reads below.
+constexpr int EPI_WARP_FLOATS = 32 * 32;
+__device__ __forceinline__ int epi_idx(int c, int r) { return c * 32 + (r ^ ((c & 7) << 2)); }
+
+// Store one warp's 32 x 32 accumulator block (lane = row, v[j] = column j)
+// to column-major FP16 C through shared memory, so global traffic is 16-byte
+// vectors (8 consecutive rows of one column per lane) instead of 2-byte
+// scalars.  `cblk` points at C element (row 0, col 0) of the block; rows /
+// cols beyond rows_valid / cols_valid are not written.  The reference
+// epilogue (Epi) is applied in FP32 and rounded once to FP16.
+__device__ __forceinline__ void epi_store_block(float* stage, const uint32_t (&v)[32], __half* cblk,
+                                                int64_t ldc, int rows_valid, int cols_valid,
+                                                const Epi& epi, int lane) {
+#pragma unroll
+  for (int c = 0; c < 32; ++c) stage[epi_idx(c, lane)] = __uint_as_float(v[c]);
+  __syncwarp();
+  const int cl = lane & 7, rg = lane >> 3;
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(cblk) & 15) == 0) && ((ldc & 7) == 0);
+  // 0: alpha == 0 (beta*C or 0), 1: beta == 0 (alpha*acc), 2: general
+  const int mode = epi.skip_ab ? 0 : (epi.beta == 0.0f ? 1 : 2);
+#pragma unroll
+  for (int cgi = 0; cgi < 4; ++cgi) {
+    const int c = cgi * 8 + cl;
+    const float4 x0 = *reinterpret_cast<const float4*>(stage + epi_idx(c, rg * 8));
+    const float4 x1 = *reinterpret_cast<const float4*>(stage + epi_idx(c, rg * 8 + 4));
+    if (c < cols_valid && rg * 8 < rows_valid) {
+      __half* dst = cblk + static_cast<int64_t>(c) * ldc + rg * 8;
+      float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+      if (vec_ok && rg * 8 + 8 <= rows_valid) {
+        if (mode == 1) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) x[i] = __fmul_rn(epi.alpha, x[i]);
+        } else {
+          float cv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          if (epi.reads_c()) {
+            const uint4 raw = *reinterpret_cast<const uint4*>(dst);
+            const __half2* h2 = reinterpret_cast<const __half2*>(&raw);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 f = __half22float2(h2[i]);
+              cv[2 * i] = f.x;
+              cv[2 * i + 1] = f.y;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) x[i] = epi.apply(x[i], cv[i]);
+        }
+        uint4 out;
+        __half2* o2 = reinterpret_cast<__half2*>(&out);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o2[i] = __floats2half2_rn(x[2 * i], x[2 * i + 1]);
+        *reinterpret_cast<uint4*>(dst) = out;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (rg * 8 + i < rows_valid) {
+            const float cvs = epi.reads_c() ? __half2float(dst[i]) : 0.0f;
+            dst[i] = __float2half_rn(epi.apply(x[i], cvs));
+          }
+        }
+      }
+    }
+  }
+  __syncwarp();
+}
+
 template <int BN, bool TMA, bool A_MN, bool B_MN, bool VEC>
 __global__ void __launch_bounds__(HgCfg<BN, TMA>::THREADS, 1)
     hgemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -128,6 +200,7 @@ __global__ void __launch_bounds__(HgCfg<BN, TMA>::THREADS, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* epi_stage = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES + C::BAR_BYTES);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -139,15 +212,15 @@ __global__ void __launch_bounds__(HgCfg<BN, TMA>::THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 32 * C::EPI_WARPS);
     }
     fence_mbar_init();
   }
-  if (TMA && warp == 0 && lane == 0) {
+  if (TMA && warp == C::PROD_WARP0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
   }
-  if (warp == C::ALLOC_WARP) tmem_alloc(tmem_holder, C::TMEM_COLS);
+  if (warp == C::MMA_WARP) tmem_alloc(tmem_holder, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -155,7 +228,7 @@ __global__ void __launch_bounds__(HgCfg<BN, TMA>::THREADS, 1)
 
   const int nkb = static_cast<int>((p.k + HG_BK - 1) / HG_BK);
 
-  if (warp < C::PROD_WARPS) {
+  if (warp >= C::PROD_WARP0 && warp < C::MMA_WARP) {
     // ======================= producer =======================
     int s = 0;
     uint32_t ph = 0;
@@ -188,7 +261,7 @@ __global__ void __launch_bounds__(HgCfg<BN, TMA>::THREADS, 1)
         }
       }
     } else {
-      const int tid = threadIdx.x;  // 0..127
+      const int tid = threadIdx.x - C::PROD_WARP0 * 32;  // 0..127
       for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         int64_t z; int mt, nt;
         tile_coords(t, tiles_m, tiles_n, group_m, z, mt, nt);
@@ -244,9 +317,10 @@ __global__ void __launch_bounds__(HgCfg<BN, TMA>::THREADS, 1)
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
     }
-  } else if (warp >= C::EPI_WARP0) {
+  } else if (warp < C::EPI_WARPS) {
     // ======================= epilogue =======================
     const int quad = warp & 3;
+    const int half = warp >> 2;
     int acc = 0;
     uint32_t aph = 0;
     for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
@@ -257,29 +331,22 @@ __global__ void __launch_bounds__(HgCfg<BN, TMA>::THREADS, 1)
       epi.alpha = inst_alpha(p, z);
       epi.beta = inst_beta(p, z);
       epi.skip_ab = (epi.alpha == 0.0f);
-      const int64_t row = m0 + quad * 32 + lane;
-      const bool row_ok = row < p.m;
+      const int64_t row0 = m0 + quad * 32;
+      const int rows_valid = static_cast<int>(min64(32, p.m - row0));
       __half* Cz = static_cast<__half*>(p.c) + inst_off(p.c_off, p.stride_c, p.c_offs, z);
       const int n_left = static_cast<int>(min64(BN, p.n - n0));
+      float* stage = epi_stage + warp * EPI_WARP_FLOATS;  // one buffer per epilogue warp
 
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
-      for (int cb = 0; cb < BN / 32; ++cb) {
+      for (int cb = half * (BN / 64); cb < (half + 1) * (BN / 64); ++cb) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(t_row + cb * 32, v);
         tmem_ld_wait();
-        if (row_ok) {
-          __half* cp = Cz + (n0 + cb * 32) * p.ldc + row;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (cb * 32 + j < n_left) {
-              const float cv = epi.reads_c() ? __half2float(cp[j * p.ldc]) : 0.0f;
-              cp[j * p.ldc] = __float2half_rn(epi.apply(__uint_as_float(v[j]), cv));
-            }
-          }
-        }
+        if (rows_valid > 0 && cb * 32 < n_left)
+          epi_store_block(stage, v, Cz + (n0 + cb * 32) * p.ldc + row0, p.ldc, rows_valid, n_left - cb * 32, epi, lane);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -289,7 +356,7 @@ __global__ void __launch_bounds__(HgCfg<BN, TMA>::THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == C::ALLOC_WARP) {
+  if (warp == C::MMA_WARP) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
   }

@@ -1,0 +1,256 @@
+// hgemm_tc_small.cuh — FP16 GEMM for small instances (m, n <= 64): the
+// batched small-matrix path of BASELINE config C4 (16384 x 32^3 / 64^3).
+//
+// Replaces the reference's per-instance Python loop + one launch over all
+// work-groups (pkg/src/tunedblas/routines/extras.py:188-286; gemm_direct_tasks
+// compute.py:432-471) for small shapes.
+//
+// A 128-row UMMA tile is filled with P = 128/MI instances stacked along M
+// (rows [z*MI, z*MI+m) hold instance z's A) and the B operands of the same
+// P instances side by side along N (columns [z*NI, z*NI+n)): D = A'·B' holds
+// instance z's product in the diagonal block (z*MI, z*NI).  The off-diagonal
+// blocks are wasted tensor work (the tensor pipe has >100x headroom at these
+// arithmetic intensities — the path is HBM-bound), in exchange for P
+// instances per MMA / per epilogue / per pipeline stage.  Each output element
+// still sees exactly the K sequence of the general kernel (64-deep K blocks of
+// 4 x K16 steps, zero-filled tail) and tcgen05 results are independent of the
+// tile's N extent and neighbours (tests: test_small_path_bitwise_equals_
+// general_path), so small and general paths agree bitwise.
+//
+// Producer: 4 warps issue 16-byte cp.async (zero-fill for tails / missing
+// instances) straight into the SWIZZLE_128B layout the UMMA descriptors
+// expect, keeping DEPTH stages in flight per thread; completion is published
+// with fence.proxy.async + mbarrier arrive.  Misaligned operands take the
+// register path (8 x 2-byte loads per chunk).
+#pragma once
+
+#include "hgemm_tc.cuh"
+
+namespace tb {
+
+template <int MI, int NI>
+struct HsCfg {
+  static constexpr int P = 128 / MI;
+  static constexpr int BN = P * NI;
+  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N");
+  static constexpr int A_BYTES = 128 * HG_BK * 2;
+  static constexpr int B_BYTES = BN * HG_BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (196608 / STAGE_BYTES) > 8 ? 8 : (196608 / STAGE_BYTES);  // <= 192 KB ring
+  static constexpr int DEPTH = STAGES - 1;
+  static constexpr int ACC = (BN <= 128) ? 4 : 2;
+  static constexpr int TMEM_COLS = (ACC * BN <= 256) ? 256 : 512;
+  // warps 0-7 epilogue (TMEM quadrant w%4, column half w/4), 8-11 producer,
+  // 12 TMEM allocation + MMA issue
+  static constexpr int EPI_WARPS = 8, PROD_WARP0 = 8, MMA_WARP = 12;
+  static constexpr int THREADS = 13 * 32;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 1024 + EPI_WARPS * EPI_WARP_FLOATS * 4;
+};
+
+// Fill one packed operand tile (ROWS = 128 for A', BN for B') of 64 K.
+// ROWS are P = ROWS/SLOT instance slots of SLOT rows each; `extent` is the
+// instance's m (A) or n (B); `inst[s]` points at instance slot s's operand
+// (nullptr when the slot is past the end of the batch).
+//   K-major : chunk j of thread t = row (t>>3) + 16j, K chunk t&7;
+//   MN-major: chunk j of thread t = sub-tile j/4, K row (t>>3) + 16(j%4),
+//             MN chunk t&7.
+// With that assignment every chunk's slot and smem offset is a compile-time
+// function of j plus a per-thread constant, so the loop body is a handful of
+// integer ops and one cp.async.
+template <int ROWS, int SLOT, bool MN, bool VEC>
+__device__ __forceinline__ void small_fill(uint8_t* smem, const __half* const (&inst)[4], const __half* any,
+                                           int64_t ld, int extent, int64_t k0, int k_left, int tid) {
+  constexpr int PER_T = ROWS * 8 / 128;
+  const int q = tid >> 3;   // 0..15
+  const int c = tid & 7;    // 16-byte chunk within a 128-byte row
+  const uint32_t off0 = static_cast<uint32_t>((q >> 3) * 1024 + (q & 7) * 128 + ((c ^ (q & 7)) << 4));
+#pragma unroll
+  for (int j = 0; j < PER_T; ++j) {
+    int slot, idx, valid;
+    int64_t eoff;
+    uint32_t off;
+    if (!MN) {
+      slot = (16 * j) / SLOT;
+      idx = q + (16 * j) % SLOT;
+      valid = (idx < extent) ? min(8, k_left - c * 8) : 0;
+      eoff = static_cast<int64_t>(idx) * ld + k0 + c * 8;
+      off = off0 + j * 2048;
+    } else {
+      const int sub = j >> 2;
+      const int mn = sub * 64 + c * 8;
+      slot = mn / SLOT;
+      idx = mn % SLOT;
+      const int r = q + 16 * (j & 3);
+      valid = (r < k_left) ? min(8, extent - idx) : 0;
+      eoff = (k0 + r) * ld + idx;
+      off = off0 + sub * 8192 + (j & 3) * 2048;
+    }
+    const __half* base = inst[slot];
+    if (base == nullptr || valid < 0) valid = 0;
+    const __half* src = valid > 0 ? base + eoff : any;
+    if (VEC) {
+      cp_async_16(smem + off, src, static_cast<uint32_t>(valid) * 2u);
+    } else {
+      const uint4 v = (valid > 0) ? ldg_chunk8<false>(src, valid) : make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4*>(smem + off) = v;
+    }
+  }
+}
+
+template <int MI, int NI, bool A_MN, bool B_MN, bool VEC>
+__global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
+    hgemm_tc_small_kernel(Problem p, int64_t total_tiles) {
+  using C = HsCfg<MI, NI>;
+  constexpr int STAGES = C::STAGES, P = C::P, BN = C::BN, ACC = C::ACC;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + ACC;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + ACC);
+  float* epi_stage = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES + 1024);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < ACC; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 32 * C::EPI_WARPS);
+    }
+    fence_mbar_init();
+  }
+  if (warp == C::MMA_WARP) tmem_alloc(tmem_holder, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int nkb = static_cast<int>((p.k + HG_BK - 1) / HG_BK);
+  const int m = static_cast<int>(p.m), n = static_cast<int>(p.n);
+
+  if (warp >= C::PROD_WARP0 && warp < C::MMA_WARP) {
+    // ===================== producer (cp.async ring) =====================
+    const int tid = threadIdx.x - C::PROD_WARP0 * 32;
+    const __half* A = static_cast<const __half*>(p.a);
+    const __half* B = static_cast<const __half*>(p.b);
+    int64_t it = 0;
+    for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      const int64_t zbase = t * P;
+      const __half* ia[4];
+      const __half* ib[4];
+#pragma unroll
+      for (int sl = 0; sl < 4; ++sl) {
+        const int64_t zi = zbase + sl;
+        const bool ok = sl < P && zi < p.batch;
+        ia[sl] = ok ? A + inst_off(p.a_off, p.stride_a, p.a_offs, zi) : nullptr;
+        ib[sl] = ok ? B + inst_off(p.b_off, p.stride_b, p.b_offs, zi) : nullptr;
+      }
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = static_cast<int>(it % STAGES);
+        const uint32_t ph = static_cast<uint32_t>((it / STAGES) & 1);
+        mbar_wait(&empty[s], ph ^ 1);
+        const int64_t k0 = static_cast<int64_t>(kb) * HG_BK;
+        const int k_left = static_cast<int>(min64(HG_BK, p.k - k0));
+        if (!(p.dbg & 2)) {
+        small_fill<128, MI, A_MN, VEC>(sA + s * C::A_BYTES, ia, A, p.lda, m, k0, k_left, tid);
+        small_fill<BN, NI, B_MN, VEC>(sB + s * C::B_BYTES, ib, B, p.ldb, n, k0, k_left, tid);
+        }
+        if (VEC) {
+          cp_async_commit();
+          if (it >= C::DEPTH - 1) {
+            cp_async_wait<C::DEPTH - 1>();
+            fence_proxy_async_smem();
+            mbar_arrive(&full[(it - (C::DEPTH - 1)) % STAGES]);
+          }
+        } else {
+          fence_proxy_async_smem();
+          mbar_arrive(&full[s]);
+        }
+        ++it;
+      }
+    }
+    if (VEC) {
+      cp_async_wait<0>();
+      fence_proxy_async_smem();
+      for (int64_t j = (it > C::DEPTH - 1 ? it - (C::DEPTH - 1) : 0); j < it; ++j) mbar_arrive(&full[j % STAGES]);
+    }
+  } else if (warp == C::MMA_WARP) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_f16(128, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      int64_t it = 0, tile_i = 0;
+      for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tile_i) {
+        const int acc = static_cast<int>(tile_i % ACC);
+        mbar_wait(&tempty[acc], static_cast<uint32_t>(((tile_i / ACC) & 1) ^ 1));
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = static_cast<int>(it % STAGES);
+          mbar_wait(&full[s], static_cast<uint32_t>((it / STAGES) & 1));
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + s * C::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + s * C::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < HG_BK / 16; ++kk) {
+            const uint64_t adesc = A_MN ? umma_desc_sw128(a_addr + kk * 2048, 8192, 1024)
+                                        : umma_desc_sw128(a_addr + kk * 32, 16, 1024);
+            const uint64_t bdesc = B_MN ? umma_desc_sw128(b_addr + kk * 2048, 8192, 1024)
+                                        : umma_desc_sw128(b_addr + kk * 32, 16, 1024);
+            if (!(p.dbg & 4)) tc_mma_f16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          tc_commit(&empty[s]);
+        }
+        tc_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp < C::EPI_WARPS) {
+    // ===================== epilogue =====================
+    const int quad = warp & 3;
+    const int half = warp >> 2;
+    const int slot = (quad * 32) / MI;
+    int64_t tile_i = 0;
+    for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tile_i) {
+      const int acc = static_cast<int>(tile_i % ACC);
+      const int64_t zi = t * P + slot;
+      const bool inst_ok = zi < p.batch;
+      Epi epi;
+      epi.alpha = inst_ok ? inst_alpha(p, zi) : 0.0f;
+      epi.beta = inst_ok ? inst_beta(p, zi) : 0.0f;
+      epi.skip_ab = (epi.alpha == 0.0f);
+      __half* Cz = static_cast<__half*>(p.c) + (inst_ok ? inst_off(p.c_off, p.stride_c, p.c_offs, zi) : 0);
+      const int row0 = quad * 32 - slot * MI;           // first instance row of this warp
+      const int rows_valid = inst_ok ? min(32, m - row0) : 0;
+      float* stage = epi_stage + warp * EPI_WARP_FLOATS;  // one buffer per epilogue warp
+      mbar_wait(&tfull[acc], static_cast<uint32_t>((tile_i / ACC) & 1));
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                             static_cast<uint32_t>(acc * BN + slot * NI);
+      // NI = 64: each column half takes one 32-column chunk; NI = 32: half 0 only
+#pragma unroll
+      for (int cb = half; cb < NI / 32; cb += 2) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_row + cb * 32, v);
+        tmem_ld_wait();
+        if (rows_valid > 0 && cb * 32 < n && !(p.dbg & 1))
+          epi_store_block(stage, v, Cz + static_cast<int64_t>(cb * 32) * p.ldc + row0, p.ldc, rows_valid,
+                          n - cb * 32, epi, lane);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == C::MMA_WARP) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+}  // namespace tb

@@ -1,0 +1,249 @@
+// sgemm_small.cuh — FP32 GEMM for small instances (m <= MI, n <= NI), the
+// batched small-matrix path (BASELINE config C4) on the FFMA pipe.
+//
+// Persistent CTAs of 256 threads stream "stages" = (group of G instances,
+// 32-deep K chunk) through a STAGES-deep cp.async ring in shared memory
+// (Ampere-style multistage main loop: wait oldest group, barrier, refill the
+// slot just freed, compute).  G = 256*16 / (MI*NI) instances share a stage,
+// each computed by MI*NI/16 threads with a 4x4 register micro-tile.
+//
+// Operands keep their global major-ness in shared memory (cp.async moves
+// 16-byte chunks along the contiguous dimension, zero-filling tails); the
+// compute loop reads 128-bit fragments along M/N for MN-contiguous operands
+// and along K (4 k-steps at a time) for K-contiguous ones.  Each output
+// element is the same sequential-k FMA chain as every other SGEMM kernel
+// (exactly k FMAs in ascending k; the zero-filled tail is never multiplied),
+// so results are bitwise identical to sgemm_simt and the C oracle.
+#pragma once
+
+#include "common.cuh"
+
+namespace tb {
+
+template <int MI, int NI>
+struct SsCfg {
+  static constexpr int KC = 32;
+  static constexpr int TY = MI / 4, TX = NI / 4;        // threads per instance = TX*TY
+  static constexpr int TPI = TX * TY;
+  static constexpr int G = 256 / TPI;                   // instances per stage
+  // smem per instance slot: A as [KC][MI] (M-contig) or [MI][KC] with the
+  // 16-byte chunks XOR-swizzled by (row/4)%8 (K-contig, conflict-free reads)
+  static constexpr int A_ELEMS = KC * MI;
+  static constexpr int B_ELEMS = KC * NI;
+  static constexpr int STAGE_FLOATS = G * (A_ELEMS + B_ELEMS);
+  // 32x32: 3 stages of 32 KB -> 2 CTAs/SM; 64x64: 4 stages of 16 KB -> 3 CTAs/SM
+  static constexpr int STAGES = (4 * STAGE_FLOATS * 4 <= 72 * 1024) ? 4 : 3;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_FLOATS * 4;
+};
+
+template <int MI, int NI, bool AK, bool BNC>
+__global__ void __launch_bounds__(256, 1)
+    sgemm_small_kernel(Problem p, int64_t groups) {
+  using C = SsCfg<MI, NI>;
+  constexpr int KC = C::KC, G = C::G, STAGES = C::STAGES;
+  // K-contiguous slot layout: element (row, kk) of a [rows][KC] tile
+  auto kidx = [](int row, int kk) {
+    return row * KC + ((((kk >> 2) ^ ((row >> 2) & 7)) << 2) | (kk & 3));
+  };
+  extern __shared__ __align__(16) float smem_f[];
+
+  const int tid = threadIdx.x;
+  const int slot = tid / C::TPI;
+  const int lt = tid % C::TPI;
+  const int ty = lt % C::TY, tx = lt / C::TY;
+  const int m = static_cast<int>(p.m), n = static_cast<int>(p.n);
+  const int kchunks = static_cast<int>((p.k + KC - 1) / KC);
+  const float* A = static_cast<const float*>(p.a);
+  const float* B = static_cast<const float*>(p.b);
+
+  // Stage sequence of this CTA: (group gi, chunk kc), gi = blockIdx.x + j*gridDim.x
+  const int64_t my_groups = (groups - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const int64_t total = my_groups * kchunks;
+
+  auto stage_ptr = [&](int s) { return smem_f + s * C::STAGE_FLOATS; };
+
+  // Issue the cp.async copies of stage index `si` into ring slot `s`.
+  // Chunk j of thread t is element chunk e = t + 256 j of the stage; since
+  // every per-instance chunk count is a multiple of 256 the instance slot of
+  // chunk j is a compile-time constant and its position a per-thread
+  // constant, so only the instance pointers are computed per stage.
+  constexpr int A_CH = MI * KC / 4, B_CH = NI * KC / 4;
+  static_assert(A_CH % 256 == 0 && B_CH % 256 == 0, "whole chunks per thread");
+  auto issue = [&](int64_t si, int s) {
+    const int64_t gi = blockIdx.x + (si / kchunks) * gridDim.x;
+    const int kc = static_cast<int>(si % kchunks);
+    const int64_t k0 = static_cast<int64_t>(kc) * KC;
+    const int k_left = static_cast<int>(min64(KC, p.k - k0));
+    float* st = stage_ptr(s);
+    const float* ia[G];
+    const float* ib[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int64_t z = gi * G + g;
+      ia[g] = z < p.batch ? A + inst_off(p.a_off, p.stride_a, p.a_offs, z) : nullptr;
+      ib[g] = z < p.batch ? B + inst_off(p.b_off, p.stride_b, p.b_offs, z) : nullptr;
+    }
+#pragma unroll
+    for (int j = 0; j < G * A_CH / 256; ++j) {
+      const int g = (256 * j) / A_CH;
+      const int r = (256 * j) % A_CH + tid;
+      int row, kk;
+      if (AK) { row = r / (KC / 4); kk = (r % (KC / 4)) * 4; }
+      else { kk = r / (MI / 4); row = (r % (MI / 4)) * 4; }
+      int valid;
+      int64_t eoff;
+      if (AK) {
+        valid = (row < m) ? max(0, min(4, k_left - kk)) : 0;
+        eoff = static_cast<int64_t>(row) * p.lda + k0 + kk;
+      } else {
+        valid = (kk < k_left) ? max(0, min(4, m - row)) : 0;
+        eoff = (k0 + kk) * p.lda + row;
+      }
+      if (ia[g] == nullptr) valid = 0;
+      float* dst = st + g * C::A_ELEMS + (AK ? kidx(row, kk) : kk * MI + row);
+      cp_async_16(dst, valid > 0 ? ia[g] + eoff : A, static_cast<uint32_t>(valid) * 4u);
+    }
+#pragma unroll
+    for (int j = 0; j < G * B_CH / 256; ++j) {
+      const int g = (256 * j) / B_CH;
+      const int r = (256 * j) % B_CH + tid;
+      int col, kk;
+      if (!BNC) { col = r / (KC / 4); kk = (r % (KC / 4)) * 4; }   // K-contiguous
+      else { kk = r / (NI / 4); col = (r % (NI / 4)) * 4; }         // N-contiguous
+      int valid;
+      int64_t eoff;
+      if (!BNC) {
+        valid = (col < n) ? max(0, min(4, k_left - kk)) : 0;
+        eoff = static_cast<int64_t>(col) * p.ldb + k0 + kk;
+      } else {
+        valid = (kk < k_left) ? max(0, min(4, n - col)) : 0;
+        eoff = (k0 + kk) * p.ldb + col;
+      }
+      if (ib[g] == nullptr) valid = 0;
+      float* dst = st + G * C::A_ELEMS + g * C::B_ELEMS + (!BNC ? kidx(col, kk) : kk * NI + col);
+      cp_async_16(dst, valid > 0 ? ib[g] + eoff : B, static_cast<uint32_t>(valid) * 4u);
+    }
+  };
+
+  // prologue: STAGES-1 stages in flight
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < total) issue(s, s);
+    cp_async_commit();
+  }
+
+  float acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0f;
+
+  for (int64_t si = 0; si < total; ++si) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    // refill the slot consumed in the previous iteration
+    const int64_t nxt = si + STAGES - 1;
+    if (nxt < total) issue(nxt, static_cast<int>(nxt % STAGES));
+    cp_async_commit();
+
+    const int s = static_cast<int>(si % STAGES);
+    const int kc = static_cast<int>(si % kchunks);
+    const int64_t gi = blockIdx.x + (si / kchunks) * gridDim.x;
+    const int k_left = static_cast<int>(min64(KC, p.k - static_cast<int64_t>(kc) * KC));
+    const float* as = stage_ptr(s) + slot * C::A_ELEMS;
+    const float* bs = stage_ptr(s) + G * C::A_ELEMS + slot * C::B_ELEMS;
+    const int r0 = ty * 4, c0 = tx * 4;
+
+    int kk = 0;
+    for (; kk + 4 <= k_left; kk += 4) {
+      float a[4][4], b[4][4];  // [k][row], [k][col]
+      if (AK) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const float4 t = *reinterpret_cast<const float4*>(as + kidx(r0 + r, kk));
+          a[0][r] = t.x; a[1][r] = t.y; a[2][r] = t.z; a[3][r] = t.w;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 t = *reinterpret_cast<const float4*>(as + (kk + q) * MI + r0);
+          a[q][0] = t.x; a[q][1] = t.y; a[q][2] = t.z; a[q][3] = t.w;
+        }
+      }
+      if (!BNC) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float4 t = *reinterpret_cast<const float4*>(bs + kidx(c0 + c, kk));
+          b[0][c] = t.x; b[1][c] = t.y; b[2][c] = t.z; b[3][c] = t.w;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 t = *reinterpret_cast<const float4*>(bs + (kk + q) * NI + c0);
+          b[q][0] = t.x; b[q][1] = t.y; b[q][2] = t.z; b[q][3] = t.w;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[r][c] = __fmaf_rn(a[q][r], b[q][c], acc[r][c]);
+    }
+    for (; kk < k_left; ++kk) {  // K tail: exactly the remaining FMAs
+      float a[4], b[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = AK ? as[kidx(r0 + r, kk)] : as[kk * MI + r0 + r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) b[c] = !BNC ? bs[kidx(c0 + c, kk)] : bs[kk * NI + c0 + c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = __fmaf_rn(a[r], b[c], acc[r][c]);
+    }
+
+    if (kc == kchunks - 1) {
+      // epilogue for this thread's instance, then reset the accumulators
+      const int64_t z = gi * G + slot;
+      if (z < p.batch) {
+        Epi epi;
+        epi.alpha = inst_alpha(p, z);
+        epi.beta = inst_beta(p, z);
+        epi.skip_ab = (epi.alpha == 0.0f) || (p.k == 0);
+        const int64_t coff = inst_off(p.c_off, p.stride_c, p.c_offs, z);
+        float* Cz = static_cast<float*>(p.c) + coff;
+        const bool cvec = ((coff & 3) == 0) && ((p.ldc & 3) == 0) && (r0 + 3 < m);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int col = c0 + c;
+          if (col >= n) continue;
+          float* cc = Cz + static_cast<int64_t>(col) * p.ldc + r0;
+          if (cvec) {
+            float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (epi.reads_c()) cv = *reinterpret_cast<const float4*>(cc);
+            float4 o;
+            o.x = epi.apply(acc[0][c], cv.x);
+            o.y = epi.apply(acc[1][c], cv.y);
+            o.z = epi.apply(acc[2][c], cv.z);
+            o.w = epi.apply(acc[3][c], cv.w);
+            *reinterpret_cast<float4*>(cc) = o;
+          } else {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              if (r0 + r < m) {
+                const float cv = epi.reads_c() ? cc[r] : 0.0f;
+                cc[r] = epi.apply(acc[r][c], cv);
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = 0.0f;
+    }
+  }
+  cp_async_wait<0>();
+}
+
+}  // namespace tb

@@ -15,11 +15,14 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include "hgemm_tc.cuh"
+#include "hgemm_tc_small.cuh"
 #include "sgemm_simt.cuh"
+#include "sgemm_small.cuh"
 #include "tbgemm.h"
 
 using namespace tb;
@@ -176,6 +179,43 @@ int launch_simt(const Call& c, const char* tag) {
   return check_launch("sgemm_simt launch");
 }
 
+template <int MI, int NI, bool AK, bool BNC>
+int launch_ss(const Call& c) {
+  using Cfg = SsCfg<MI, NI>;
+  const Problem& p = c.p;
+  const int64_t groups = (p.batch + Cfg::G - 1) / Cfg::G;
+  auto kern = sgemm_small_kernel<MI, NI, AK, BNC>;
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) {
+      set_err("cudaFuncSetAttribute", e);
+      return TB_ERR_CUDA;
+    }
+    int v = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, 256, Cfg::SMEM_BYTES) != cudaSuccess || v < 1) v = 1;
+    per_sm = v;
+  }
+  const int sms = sm_count() > 0 ? sm_count() : 148;
+  const int64_t cap = static_cast<int64_t>(sms) * per_sm;
+  const int64_t g = groups < cap ? groups : cap;
+  dim3 grid(static_cast<unsigned>(g)), block(256);
+  kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(p, groups);
+  char name[64];
+  snprintf(name, sizeof(name), "sgemm_small_%dx%d_g%d_%c%c", MI, NI, Cfg::G, AK ? 'k' : 'm', BNC ? 'n' : 'k');
+  record(name, grid, block, 1, Cfg::SMEM_BYTES, groups);
+  return check_launch("sgemm_small launch");
+}
+
+template <int MI, int NI>
+int launch_ss_layout(const Call& c) {
+  const bool ak = c.p.a_kcontig, bnc = c.p.b_ncontig;
+  if (!ak && !bnc) return launch_ss<MI, NI, false, false>(c);
+  if (!ak && bnc) return launch_ss<MI, NI, false, true>(c);
+  if (ak && !bnc) return launch_ss<MI, NI, true, false>(c);
+  return launch_ss<MI, NI, true, true>(c);
+}
+
 int dispatch_sgemm(const Call& c) {
   const Problem& p = c.p;
   if (c.flags & TB_FLAG_TF32) {
@@ -202,6 +242,11 @@ int dispatch_sgemm(const Call& c) {
     if (c.params->VWM == 1 && c.params->VWN == 1) vec = false;
   }
   if (!vec) return launch_simt<64, 64, 16, 4, 4, false, 2>(c, "general");
+  // Small instances: persistent cp.async-pipelined kernel (bitwise identical).
+  if (p.k > 0 && p.m <= 64 && p.n <= 64 && (p.batch > 1 || p.k <= 4096)) {
+    if (p.m <= 32 && p.n <= 32) return launch_ss_layout<32, 32>(c);
+    return launch_ss_layout<64, 64>(c);
+  }
   const int sms = sm_count() > 0 ? sm_count() : 148;
   const int64_t tiles128 = ((p.m + 127) / 128) * ((p.n + 127) / 128) * p.batch;
   if (p.m <= 32 && p.n <= 32) return launch_simt<32, 32, 32, 4, 4, true, 8>(c, "32");
@@ -215,6 +260,18 @@ int dispatch_sgemm(const Call& c) {
 // ---------------------------------------------------------------------------
 // HGEMM dispatch
 // ---------------------------------------------------------------------------
+bool hgemm_aligned(const Call& c) {
+  const Problem& p = c.p;
+  bool al = (p.lda % 8 == 0) && (p.ldb % 8 == 0) && aligned_elems(p.a, 0, 2, 16) && aligned_elems(p.b, 0, 2, 16);
+  if (p.a_offs || p.b_offs) {
+    al = al && c.offs_aligned;
+  } else {
+    al = al && (p.a_off % 8 == 0) && (p.b_off % 8 == 0);
+    if (p.batch > 1) al = al && (p.stride_a % 8 == 0) && (p.stride_b % 8 == 0);
+  }
+  return al;
+}
+
 template <int BN, bool TMA, bool AMN, bool BMN, bool VEC>
 int launch_hg(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
   using Cfg = HgCfg<BN, TMA>;
@@ -257,15 +314,8 @@ template <int BN>
 int dispatch_hgemm_bn(const Call& c) {
   const Problem& p = c.p;
   const bool amn = !p.a_kcontig, bmn = p.b_ncontig;
-  // 16-byte alignment of every operand row start (TMA and LDG.128).
-  bool al = (p.lda % 8 == 0) && (p.ldb % 8 == 0) && aligned_elems(p.a, 0, 2, 16) && aligned_elems(p.b, 0, 2, 16);
-  bool generic = (p.a_offs != nullptr) || (p.b_offs != nullptr);
-  if (generic) {
-    al = al && c.offs_aligned;
-  } else {
-    al = al && (p.a_off % 8 == 0) && (p.b_off % 8 == 0);
-    if (p.batch > 1) al = al && (p.stride_a % 8 == 0) && (p.stride_b % 8 == 0);
-  }
+  const bool al = hgemm_aligned(c);
+  const bool generic = (p.a_offs != nullptr) || (p.b_offs != nullptr);
   const bool big = p.m < (1LL << 31) && p.n < (1LL << 31) && p.k < (1LL << 31) && p.batch < (1LL << 31);
   CUtensorMap ta, tbm;
   memset(&ta, 0, sizeof(ta));
@@ -286,7 +336,56 @@ int dispatch_hgemm_bn(const Call& c) {
   return launch_hg_layout<BN, false, false>(c, ta, tbm);
 }
 
+template <int MI, int NI, bool AMN, bool BMN, bool VEC>
+int launch_hs(const Call& c) {
+  using Cfg = HsCfg<MI, NI>;
+  const Problem& p = c.p;
+  const int64_t total = (p.batch + Cfg::P - 1) / Cfg::P;
+  auto kern = hgemm_tc_small_kernel<MI, NI, AMN, BMN, VEC>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) {
+      set_err("cudaFuncSetAttribute", e);
+      return TB_ERR_CUDA;
+    }
+    attr_set = true;
+  }
+  const int sms = sm_count() > 0 ? sm_count() : 148;
+  const int64_t g = total < sms ? total : sms;
+  dim3 grid(static_cast<unsigned>(g)), block(Cfg::THREADS);
+  kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(p, total);
+  char name[64];
+  snprintf(name, sizeof(name), "hgemm_tc_small_%dx%d_p%d_%c%c%s", MI, NI, Cfg::P, AMN ? 'm' : 'k',
+           BMN ? 'n' : 'k', VEC ? "_cpasync" : "_scalar");
+  record(name, grid, block, 1, Cfg::SMEM_BYTES, total);
+  return check_launch("hgemm_tc_small launch");
+}
+
+template <int MI, int NI, bool VEC>
+int launch_hs_layout(const Call& c) {
+  const bool amn = !c.p.a_kcontig, bmn = c.p.b_ncontig;
+  if (!amn && !bmn) return launch_hs<MI, NI, false, false, VEC>(c);
+  if (!amn && bmn) return launch_hs<MI, NI, false, true, VEC>(c);
+  if (amn && !bmn) return launch_hs<MI, NI, true, false, VEC>(c);
+  return launch_hs<MI, NI, true, true, VEC>(c);
+}
+
+template <bool VEC>
+int dispatch_hsmall(const Call& c) {
+  const Problem& p = c.p;
+  if (p.m <= 32) return p.n <= 32 ? launch_hs_layout<32, 32, VEC>(c) : launch_hs_layout<32, 64, VEC>(c);
+  return p.n <= 32 ? launch_hs_layout<64, 32, VEC>(c) : launch_hs_layout<64, 64, VEC>(c);
+}
+
 int dispatch_hgemm(const Call& c) {
+  // Small instances (m, n <= 64): packed tcgen05 kernel.  Bitwise identical to
+  // the general kernel (same per-element K sequence), so this is a pure
+  // function of the shape and single / batched calls stay consistent.
+  if (c.p.m <= 64 && c.p.n <= 64 && !(c.flags & TB_FLAG_NO_PACK)) {
+    if (hgemm_aligned(c)) return dispatch_hsmall<true>(c);
+    return dispatch_hsmall<false>(c);
+  }
   if (c.flags & TB_FLAG_TF32) {
     snprintf(g_last_err, sizeof(g_last_err), "TF32 flag applies to SGEMM only");
     return TB_ERR_UNSUPPORTED;
@@ -339,6 +438,8 @@ Call make_call(int prec, int layout, int ta, int tbt, int64_t m, int64_t n, int6
   c.flags = flags;
   c.stream = static_cast<cudaStream_t>(stream);
   c.p.batch = 1;
+  const char* dbg = getenv("TBGEMM_DBG");
+  c.p.dbg = dbg ? atoi(dbg) : 0;
   return c;
 }
 

@@ -42,10 +42,18 @@ def require_gpu(ctx: Context) -> None:
             "— there is no CPU fallback")
 
 
+_PARAM_STRUCTS: dict = {}
+
+
 def _params(config: Configuration | None):
     if config is None:
         return None
-    return ctypes.byref(native.TbGemmParams.from_dict(config.as_dict()))
+    st = _PARAM_STRUCTS.get(config)
+    if st is None:
+        st = native.TbGemmParams.from_dict(config.as_dict())
+        if len(_PARAM_STRUCTS) < 4096:
+            _PARAM_STRUCTS[config] = st
+    return ctypes.byref(st)
 
 
 def _stream(ctx: Context) -> int:

@@ -167,3 +167,38 @@ def test_full_size_batch_16384(ctx, prec, size):
         else:
             tol = orc.gemm_tolerance(A.reshape(m, m), B.reshape(m, m), "H").reshape(-1)
             assert orc.allclose_tol(got, want, tol, scale=2.0)
+
+
+@pytest.mark.parametrize("prec", [Precision.S, Precision.H])
+@pytest.mark.parametrize("layout", [Layout.COL_MAJOR, Layout.ROW_MAJOR])
+@pytest.mark.parametrize("ta", [Transpose.NO, Transpose.YES])
+@pytest.mark.parametrize("tbt", [Transpose.NO, Transpose.YES])
+@pytest.mark.parametrize("shape", [(32, 32, 32), (64, 64, 64), (20, 50, 77), (64, 17, 300), (8, 64, 1)])
+def test_small_path_bitwise_equals_general_path(ctx, prec, layout, ta, tbt, shape):
+    """The packed small-instance kernels (tcgen05 for H, cp.async FFMA for S)
+    give the same bits as the general kernels forced via flags."""
+    from paper_1705_05249_b200.kernels import native
+    from paper_1705_05249_b200.kernels.dispatch import gemm_strided_batched_native
+
+    m, n, k = shape
+    batch = 37
+    rng = np.random.default_rng(m * 7 + n + k)
+    ea, eb, ec = m * k, k * n, m * n
+    host = [rand_array(rng, batch * e, prec) for e in (ea, eb, ec)]
+    lda = (m if ta is NO else k) if layout is COL else (k if ta is NO else m)
+    ldb = (k if tbt is NO else n) if layout is COL else (n if tbt is NO else k)
+    ldc = m if layout is COL else n
+    outs, kernels = [], []
+    general = native.FLAG_NO_PACK if prec is Precision.H else native.FLAG_SIMT_GENERAL
+    for flags in (0, general):
+        a, b, c = (make_buffer(ctx, h, prec) for h in host)
+        rec = gemm_strided_batched_native(ctx, prec, layout, ta, tbt, m, n, k, 1.25, a, 0, lda, ea,
+                                          b, 0, ldb, eb, -0.5, c, 0, ldc, ec, batch, None, flags)
+        outs.append(tb.buffer_read(c, 0, c.length))
+        kernels.append(rec["kernel"])
+    assert "small" not in kernels[1], kernels
+    aligned = (prec is Precision.S and all(v % 4 == 0 for v in (ea, eb, lda, ldb))) or \
+        (prec is Precision.H and all(v % 8 == 0 for v in (ea, eb, lda, ldb)))
+    if aligned or prec is Precision.H:
+        assert "small" in kernels[0], kernels
+    assert outs[0].tobytes() == outs[1].tobytes(), kernels

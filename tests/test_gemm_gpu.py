@@ -214,7 +214,7 @@ def test_routing_family_and_launch_record(ctx):
         tb.gemm(ctx, Layout.COL_MAJOR, Transpose.NO, Transpose.NO, size, size, size, 1.0, a, b, 0.0, c)
         rec = ctx.last_launch
         assert rec.family == family
-        assert rec.native["launches"] == 1 and rec.native["kernel"].startswith("sgemm_simt")
+        assert rec.native["launches"] == 1 and rec.native["kernel"].startswith("sgemm_")
 
 
 def test_override_is_recorded_and_applied(ctx):
