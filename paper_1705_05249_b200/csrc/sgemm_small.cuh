@@ -20,10 +20,11 @@
 
 namespace tb {
 
-template <int MI, int NI>
+template <int MI, int NI, int TM = 4, int TN = 4>
 struct SsCfg {
   static constexpr int KC = 32;
-  static constexpr int TY = MI / 4, TX = NI / 4;        // threads per instance = TX*TY
+  static constexpr int TY = MI / TM, TX = NI / TN;      // threads per instance = TX*TY
+  static constexpr int QM = TM / 4, QN = TN / 4;        // 4x4 sub-blocks, spaced MI/QM, NI/QN
   static constexpr int TPI = TX * TY;
   static constexpr int G = 256 / TPI;                   // instances per stage
   // smem per instance slot: A as [KC][MI] (M-contig) or [MI][KC] with the
@@ -31,15 +32,16 @@ struct SsCfg {
   static constexpr int A_ELEMS = KC * MI;
   static constexpr int B_ELEMS = KC * NI;
   static constexpr int STAGE_FLOATS = G * (A_ELEMS + B_ELEMS);
-  // 32x32: 3 stages of 32 KB -> 2 CTAs/SM; 64x64: 4 stages of 16 KB -> 3 CTAs/SM
-  static constexpr int STAGES = (4 * STAGE_FLOATS * 4 <= 72 * 1024) ? 4 : 3;
+  // 3-4 stages, <= ~100 KB so two CTAs share an SM
+  static constexpr int STAGES = (4 * STAGE_FLOATS * 4 <= 100 * 1024) ? 4 : 3;
   static constexpr int SMEM_BYTES = STAGES * STAGE_FLOATS * 4;
 };
 
-template <int MI, int NI, bool AK, bool BNC>
-__global__ void __launch_bounds__(256, 1)
+template <int MI, int NI, int TM, int TN, bool AK, bool BNC>
+__global__ void __launch_bounds__(256, 2)
     sgemm_small_kernel(Problem p, int64_t groups) {
-  using C = SsCfg<MI, NI>;
+  using C = SsCfg<MI, NI, TM, TN>;
+  constexpr int QM = C::QM, QN = C::QN;
   constexpr int KC = C::KC, G = C::G, STAGES = C::STAGES;
   // K-contiguous slot layout: element (row, kk) of a [rows][KC] tile
   auto kidx = [](int row, int kk) {
@@ -131,11 +133,11 @@ __global__ void __launch_bounds__(256, 1)
     cp_async_commit();
   }
 
-  float acc[4][4];
+  float acc[TM][TN];
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+  for (int r = 0; r < TM; ++r)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0f;
+    for (int c = 0; c < TN; ++c) acc[r][c] = 0.0f;
 
   for (int64_t si = 0; si < total; ++si) {
     cp_async_wait<STAGES - 2>();
@@ -151,54 +153,60 @@ __global__ void __launch_bounds__(256, 1)
     const int k_left = static_cast<int>(min64(KC, p.k - static_cast<int64_t>(kc) * KC));
     const float* as = stage_ptr(s) + slot * C::A_ELEMS;
     const float* bs = stage_ptr(s) + G * C::A_ELEMS + slot * C::B_ELEMS;
-    const int r0 = ty * 4, c0 = tx * 4;
+    // micro-tile rows: q*(MI/QM) + ty*4 + {0..3}; cols: q*(NI/QN) + tx*4 + {0..3}
+    auto rowof = [&](int r) { return (r >> 2) * (MI / QM) + ty * 4 + (r & 3); };
+    auto colof = [&](int c) { return (c >> 2) * (NI / QN) + tx * 4 + (c & 3); };
 
     int kk = 0;
     for (; kk + 4 <= k_left; kk += 4) {
-      float a[4][4], b[4][4];  // [k][row], [k][col]
+      float a[4][TM], b[4][TN];  // [k][row], [k][col]
       if (AK) {
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const float4 t = *reinterpret_cast<const float4*>(as + kidx(r0 + r, kk));
+        for (int r = 0; r < TM; ++r) {
+          const float4 t = *reinterpret_cast<const float4*>(as + kidx(rowof(r), kk));
           a[0][r] = t.x; a[1][r] = t.y; a[2][r] = t.z; a[3][r] = t.w;
         }
       } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float4 t = *reinterpret_cast<const float4*>(as + (kk + q) * MI + r0);
-          a[q][0] = t.x; a[q][1] = t.y; a[q][2] = t.z; a[q][3] = t.w;
-        }
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int h = 0; h < QM; ++h) {
+            const float4 t = *reinterpret_cast<const float4*>(as + (kk + q) * MI + rowof(h * 4));
+            a[q][h * 4 + 0] = t.x; a[q][h * 4 + 1] = t.y; a[q][h * 4 + 2] = t.z; a[q][h * 4 + 3] = t.w;
+          }
       }
       if (!BNC) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float4 t = *reinterpret_cast<const float4*>(bs + kidx(c0 + c, kk));
+        for (int c = 0; c < TN; ++c) {
+          const float4 t = *reinterpret_cast<const float4*>(bs + kidx(colof(c), kk));
           b[0][c] = t.x; b[1][c] = t.y; b[2][c] = t.z; b[3][c] = t.w;
         }
       } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float4 t = *reinterpret_cast<const float4*>(bs + (kk + q) * NI + c0);
-          b[q][0] = t.x; b[q][1] = t.y; b[q][2] = t.z; b[q][3] = t.w;
-        }
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int h = 0; h < QN; ++h) {
+            const float4 t = *reinterpret_cast<const float4*>(bs + (kk + q) * NI + colof(h * 4));
+            b[q][h * 4 + 0] = t.x; b[q][h * 4 + 1] = t.y; b[q][h * 4 + 2] = t.z; b[q][h * 4 + 3] = t.w;
+          }
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < TM; ++r)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) acc[r][c] = __fmaf_rn(a[q][r], b[q][c], acc[r][c]);
+          for (int c = 0; c < TN; ++c) acc[r][c] = __fmaf_rn(a[q][r], b[q][c], acc[r][c]);
     }
     for (; kk < k_left; ++kk) {  // K tail: exactly the remaining FMAs
-      float a[4], b[4];
+      float a[TM], b[TN];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) a[r] = AK ? as[kidx(r0 + r, kk)] : as[kk * MI + r0 + r];
+      for (int r = 0; r < TM; ++r) a[r] = AK ? as[kidx(rowof(r), kk)] : as[kk * MI + rowof(r)];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) b[c] = !BNC ? bs[kidx(c0 + c, kk)] : bs[kk * NI + c0 + c];
+      for (int c = 0; c < TN; ++c) b[c] = !BNC ? bs[kidx(colof(c), kk)] : bs[kk * NI + colof(c)];
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
+      for (int r = 0; r < TM; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = __fmaf_rn(a[r], b[c], acc[r][c]);
+        for (int c = 0; c < TN; ++c) acc[r][c] = __fmaf_rn(a[r], b[c], acc[r][c]);
     }
 
     if (kc == kchunks - 1) {
@@ -211,36 +219,40 @@ __global__ void __launch_bounds__(256, 1)
         epi.skip_ab = (epi.alpha == 0.0f) || (p.k == 0);
         const int64_t coff = inst_off(p.c_off, p.stride_c, p.c_offs, z);
         float* Cz = static_cast<float*>(p.c) + coff;
-        const bool cvec = ((coff & 3) == 0) && ((p.ldc & 3) == 0) && (r0 + 3 < m);
+        const bool cal = ((coff & 3) == 0) && ((p.ldc & 3) == 0);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int col = c0 + c;
+        for (int c = 0; c < TN; ++c) {
+          const int col = colof(c);
           if (col >= n) continue;
-          float* cc = Cz + static_cast<int64_t>(col) * p.ldc + r0;
-          if (cvec) {
-            float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (epi.reads_c()) cv = *reinterpret_cast<const float4*>(cc);
-            float4 o;
-            o.x = epi.apply(acc[0][c], cv.x);
-            o.y = epi.apply(acc[1][c], cv.y);
-            o.z = epi.apply(acc[2][c], cv.z);
-            o.w = epi.apply(acc[3][c], cv.w);
-            *reinterpret_cast<float4*>(cc) = o;
-          } else {
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              if (r0 + r < m) {
-                const float cv = epi.reads_c() ? cc[r] : 0.0f;
-                cc[r] = epi.apply(acc[r][c], cv);
+          for (int h = 0; h < QM; ++h) {
+            const int r0 = rowof(h * 4);
+            float* cc = Cz + static_cast<int64_t>(col) * p.ldc + r0;
+            if (cal && r0 + 3 < m) {
+              float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (epi.reads_c()) cv = *reinterpret_cast<const float4*>(cc);
+              float4 o;
+              o.x = epi.apply(acc[h * 4 + 0][c], cv.x);
+              o.y = epi.apply(acc[h * 4 + 1][c], cv.y);
+              o.z = epi.apply(acc[h * 4 + 2][c], cv.z);
+              o.w = epi.apply(acc[h * 4 + 3][c], cv.w);
+              *reinterpret_cast<float4*>(cc) = o;
+            } else {
+#pragma unroll
+              for (int r = 0; r < 4; ++r) {
+                if (r0 + r < m) {
+                  const float cvs = epi.reads_c() ? cc[r] : 0.0f;
+                  cc[r] = epi.apply(acc[h * 4 + r][c], cvs);
+                }
               }
             }
           }
         }
       }
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
+      for (int r = 0; r < TM; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = 0.0f;
+        for (int c = 0; c < TN; ++c) acc[r][c] = 0.0f;
     }
   }
   cp_async_wait<0>();

@@ -179,12 +179,12 @@ int launch_simt(const Call& c, const char* tag) {
   return check_launch("sgemm_simt launch");
 }
 
-template <int MI, int NI, bool AK, bool BNC>
+template <int MI, int NI, int TM, int TN, bool AK, bool BNC>
 int launch_ss(const Call& c) {
-  using Cfg = SsCfg<MI, NI>;
+  using Cfg = SsCfg<MI, NI, TM, TN>;
   const Problem& p = c.p;
   const int64_t groups = (p.batch + Cfg::G - 1) / Cfg::G;
-  auto kern = sgemm_small_kernel<MI, NI, AK, BNC>;
+  auto kern = sgemm_small_kernel<MI, NI, TM, TN, AK, BNC>;
   static int per_sm = 0;
   if (per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
@@ -202,18 +202,19 @@ int launch_ss(const Call& c) {
   dim3 grid(static_cast<unsigned>(g)), block(256);
   kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(p, groups);
   char name[64];
-  snprintf(name, sizeof(name), "sgemm_small_%dx%d_g%d_%c%c", MI, NI, Cfg::G, AK ? 'k' : 'm', BNC ? 'n' : 'k');
+  snprintf(name, sizeof(name), "sgemm_small_%dx%d_t%dx%d_g%d_%c%c", MI, NI, TM, TN, Cfg::G, AK ? 'k' : 'm',
+           BNC ? 'n' : 'k');
   record(name, grid, block, 1, Cfg::SMEM_BYTES, groups);
   return check_launch("sgemm_small launch");
 }
 
-template <int MI, int NI>
+template <int MI, int NI, int TM, int TN>
 int launch_ss_layout(const Call& c) {
   const bool ak = c.p.a_kcontig, bnc = c.p.b_ncontig;
-  if (!ak && !bnc) return launch_ss<MI, NI, false, false>(c);
-  if (!ak && bnc) return launch_ss<MI, NI, false, true>(c);
-  if (ak && !bnc) return launch_ss<MI, NI, true, false>(c);
-  return launch_ss<MI, NI, true, true>(c);
+  if (!ak && !bnc) return launch_ss<MI, NI, TM, TN, false, false>(c);
+  if (!ak && bnc) return launch_ss<MI, NI, TM, TN, false, true>(c);
+  if (ak && !bnc) return launch_ss<MI, NI, TM, TN, true, false>(c);
+  return launch_ss<MI, NI, TM, TN, true, true>(c);
 }
 
 int dispatch_sgemm(const Call& c) {
@@ -244,13 +245,18 @@ int dispatch_sgemm(const Call& c) {
   if (!vec) return launch_simt<64, 64, 16, 4, 4, false, 2>(c, "general");
   // Small instances: persistent cp.async-pipelined kernel (bitwise identical).
   if (p.k > 0 && p.m <= 64 && p.n <= 64 && (p.batch > 1 || p.k <= 4096)) {
-    if (p.m <= 32 && p.n <= 32) return launch_ss_layout<32, 32>(c);
-    return launch_ss_layout<64, 64>(c);
+    if (p.m <= 32 && p.n <= 32) return launch_ss_layout<32, 32, 4, 4>(c);
+    return launch_ss_layout<64, 64, 8, 4>(c);
   }
   const int sms = sm_count() > 0 ? sm_count() : 148;
   const int64_t tiles128 = ((p.m + 127) / 128) * ((p.n + 127) / 128) * p.batch;
   if (p.m <= 32 && p.n <= 32) return launch_simt<32, 32, 32, 4, 4, true, 8>(c, "32");
-  if (mwg >= 128 && nwg >= 128 && tiles128 >= sms) return launch_simt<128, 128, 8, 8, 8, true, 2>(c, "128");
+  if (mwg >= 128 && nwg >= 128) {
+    // 128x256 (8x16 micro-tile) once there are >= 4 waves of it; else 128x128x16.
+    const int64_t tiles256 = ((p.m + 127) / 128) * ((p.n + 255) / 256) * p.batch;
+    if (tiles256 >= 4 * sms) return launch_simt<128, 256, 8, 8, 16, true, 1>(c, "128x256");
+    if (tiles128 >= sms) return launch_simt<128, 128, 16, 8, 8, true, 1>(c, "128");
+  }
   if (mwg >= 128 && nwg < 128 && tiles128 * 2 >= sms) return launch_simt<128, 64, 16, 8, 4, true, 2>(c, "128x64");
   if (mwg < 128 && nwg >= 128 && tiles128 * 2 >= sms) return launch_simt<64, 128, 16, 4, 8, true, 2>(c, "64x128");
   if (mwg <= 32 && nwg <= 32) return launch_simt<32, 32, 32, 4, 4, true, 8>(c, "32");
