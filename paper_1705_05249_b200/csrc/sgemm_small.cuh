@@ -157,8 +157,8 @@ __global__ void __launch_bounds__(256, 2)
     auto rowof = [&](int r) { return (r >> 2) * (MI / QM) + ty * 4 + (r & 3); };
     auto colof = [&](int c) { return (c >> 2) * (NI / QN) + tx * 4 + (c & 3); };
 
-    int kk = 0;
-    for (; kk + 4 <= k_left; kk += 4) {
+    // one 4-deep k group: fragments then 4*TM*TN FMAs in ascending k
+    auto kgroup = [&](int kk) {
       float a[4][TM], b[4][TN];  // [k][row], [k][col]
       if (AK) {
 #pragma unroll
@@ -196,6 +196,14 @@ __global__ void __launch_bounds__(256, 2)
         for (int r = 0; r < TM; ++r)
 #pragma unroll
           for (int c = 0; c < TN; ++c) acc[r][c] = __fmaf_rn(a[q][r], b[q][c], acc[r][c]);
+        };
+    int kk = 0;
+    if (k_left == KC) {
+#pragma unroll
+      for (int g4 = 0; g4 < KC; g4 += 4) kgroup(g4);   // full chunk: offsets are compile-time
+      kk = KC;
+    } else {
+      for (; kk + 4 <= k_left; kk += 4) kgroup(kk);
     }
     for (; kk < k_left; ++kk) {  // K tail: exactly the remaining FMAs
       float a[TM], b[TN];

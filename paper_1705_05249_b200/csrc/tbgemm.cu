@@ -246,7 +246,9 @@ int dispatch_sgemm(const Call& c) {
   // Small instances: persistent cp.async-pipelined kernel (bitwise identical).
   if (p.k > 0 && p.m <= 64 && p.n <= 64 && (p.batch > 1 || p.k <= 4096)) {
     if (p.m <= 32 && p.n <= 32) return launch_ss_layout<32, 32, 4, 4>(c);
-    return launch_ss_layout<64, 64, 8, 4>(c);
+    // 33..64: the tiled kernel with a 4x8 micro-tile measured faster than the
+    // cp.async small kernel for 64^3 instances (tools/sgemm_batched_variants.cu)
+    return launch_simt<64, 64, 16, 4, 8, true, 2>(c, "64x64 4x8");
   }
   const int sms = sm_count() > 0 ? sm_count() : 148;
   const int64_t tiles128 = ((p.m + 127) / 128) * ((p.n + 127) / 128) * p.batch;
@@ -401,8 +403,15 @@ int dispatch_hgemm(const Call& c) {
   // the same MMA sequence (bitwise batched == looped).
   int nwg = 128;
   if (c.params) nwg = c.params->NWG;
-  if (nwg >= 128) return dispatch_hgemm_bn<256>(c);
-  if (nwg >= 64) return dispatch_hgemm_bn<128>(c);
+  int bn = nwg >= 128 ? 256 : (nwg >= 64 ? 128 : 64);
+  // Fewer tiles than SMs: narrow the UMMA N extent (results are independent
+  // of it — tests/test_gemm_gpu.py) so more CTAs share the work.
+  const int sms = sm_count() > 0 ? sm_count() : 148;
+  const Problem& p = c.p;
+  auto tiles = [&](int b) { return ((p.m + HG_BM - 1) / HG_BM) * ((p.n + b - 1) / b) * p.batch; };
+  while (bn > 64 && tiles(bn) < sms) bn /= 2;
+  if (bn == 256) return dispatch_hgemm_bn<256>(c);
+  if (bn == 128) return dispatch_hgemm_bn<128>(c);
   return dispatch_hgemm_bn<64>(c);
 }
 
