@@ -66,7 +66,8 @@ enum {
   TB_FLAG_TF32 = 1,        /* opt-in TF32 tensor-core SGEMM (separate tolerance) */
   TB_FLAG_NO_TMA = 2,      /* HGEMM: force the LDG producer (testing)          */
   TB_FLAG_SIMT_GENERAL = 4, /* SGEMM: force the general predicated kernel        */
-  TB_FLAG_NO_PACK = 8        /* HGEMM: no small-instance packing (testing)        */
+  TB_FLAG_NO_PACK = 8,       /* HGEMM: no small-instance packing (testing)        */
+  TB_FLAG_NO_2SM = 16        /* HGEMM: no CTA-pair (cta_group::2) kernel (testing) */
 };
 
 /*

@@ -1,0 +1,250 @@
+// hgemm_tc_2sm.cuh — FP16 GEMM on CTA pairs: tcgen05.mma.cta_group::2.
+//
+// Same contract as hgemm_tc_kernel (hgemm_tc.cuh) for large, 16-byte aligned
+// problems, re-tiled for the Blackwell 2-SM UMMA: a cluster of two CTAs on
+// one TPC computes a 256 x 256 output tile.  CTA r (r = cluster rank) loads
+// A rows [m0 + 128 r, +128) and B columns [n0 + 128 r, +128) — half of each
+// operand — and the leader's single MMA thread issues
+//   tcgen05.mma.cta_group::2.kind::f16  (M = 256, N = 256, K = 16)
+// which makes each SM multiply its own A half by BOTH B halves (the pair
+// exchanges B internally).  Per FLOP this is 1/3 less shared-memory fill and
+// L2 traffic than the 128 x 256 single-CTA tile, which under the 1 kW power
+// cap buys clock.
+//
+// Synchronisation across the pair:
+//   * both CTAs' TMA loads complete_tx on the LEADER's full[s] barrier
+//     (.cta_group::2 TMA with the peer bit masked off the mbarrier address);
+//     the leader's producer posts expect_tx for both halves;
+//   * the leader's tcgen05.commit multicasts to empty[s] / tfull[a] in both
+//     CTAs (cta mask 0b11);
+//   * both CTAs' epilogue threads arrive on the leader's tempty[a]
+//     (mapa + mbarrier.arrive.shared::cluster).
+// Each CTA's TMEM holds its 128 rows x 256 FP32 columns (double-buffered);
+// its 8 epilogue warps store them exactly as the single-CTA kernel does.
+#pragma once
+
+#include "hgemm_tc.cuh"
+
+namespace tb {
+
+constexpr int H2_BN = 256;          // pair tile N (per-CTA B half = 128)
+constexpr int H2_STAGES = 6;
+
+struct H2Cfg {
+  static constexpr int A_BYTES = 128 * HG_BK * 2;            // 16 KB: own 128 A rows
+  static constexpr int B_BYTES = (H2_BN / 2) * HG_BK * 2;    // 16 KB: own 128 B columns
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int EPI_WARPS = 8, PROD_WARP = 8, MMA_WARP = 9;
+  static constexpr int THREADS = 10 * 32;
+  static constexpr int TMEM_COLS = 512;                       // 2 x 256 accumulators
+  static constexpr int BAR_BYTES = 1024;
+  static constexpr int EPI_BYTES = EPI_WARPS * EPI_WARP_FLOATS * 4;
+  static constexpr int SMEM_BYTES = 1024 + H2_STAGES * STAGE_BYTES + BAR_BYTES + EPI_BYTES;
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 2-SM TMA: data lands in this CTA's smem, transaction bytes go to the
+// leader CTA's barrier at the same offset.
+__device__ __forceinline__ void tma_load_3d_2sm(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
+                                                int c2) {
+  const uint32_t bar_leader = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_leader), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc2_mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc2_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 rem;\n\t"
+      "mapa.shared::cluster.u32 rem, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [rem];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
+    hgemm_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Problem p,
+                        int tiles_m, int tiles_n, int group_m, int64_t total_tiles) {
+  using C = H2Cfg;
+  constexpr int STAGES = H2_STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* epi_stage = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES + C::BAR_BYTES);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int64_t cluster_id = blockIdx.x >> 1;
+  const int64_t n_clusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * 32 * C::EPI_WARPS);
+    }
+    fence_mbar_init();
+  }
+  if (warp == C::PROD_WARP && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == C::MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int nkb = static_cast<int>((p.k + HG_BK - 1) / HG_BK);
+
+  if (warp == C::PROD_WARP) {
+    // =============== producer (both CTAs: own A half + own B half) ===============
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = cluster_id; t < total_tiles; t += n_clusters) {
+        int64_t z; int mt, nt;
+        tile_coords(t, tiles_m, tiles_n, group_m, z, mt, nt);
+        const int m0 = mt * 256 + static_cast<int>(rank) * 128;
+        const int n0 = nt * H2_BN + static_cast<int>(rank) * (H2_BN / 2);
+        const int zz = static_cast<int>(z);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[s], 2 * C::STAGE_BYTES);
+          const int k0 = kb * HG_BK;
+          uint8_t* a_dst = sA + s * C::A_BYTES;
+          uint8_t* b_dst = sB + s * C::B_BYTES;
+          if (!A_MN) {
+            tma_load_3d_2sm(a_dst, &tmA, &full[s], k0, m0, zz);
+          } else {
+            tma_load_3d_2sm(a_dst, &tmA, &full[s], m0, k0, zz);
+            tma_load_3d_2sm(a_dst + 8192, &tmA, &full[s], m0 + 64, k0, zz);
+          }
+          if (!B_MN) {
+            tma_load_3d_2sm(b_dst, &tmB, &full[s], k0, n0, zz);
+          } else {
+            tma_load_3d_2sm(b_dst, &tmB, &full[s], n0, k0, zz);
+            tma_load_3d_2sm(b_dst + 8192, &tmB, &full[s], n0 + 64, k0, zz);
+          }
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == C::MMA_WARP) {
+    // =============== MMA issuer (leader CTA only) ===============
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_f16(256, H2_BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int64_t t = cluster_id; t < total_tiles; t += n_clusters) {
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * H2_BN);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + s * C::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + s * C::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < HG_BK / 16; ++kk) {
+            const uint64_t adesc = A_MN ? umma_desc_sw128(a_addr + kk * 2048, 8192, 1024)
+                                        : umma_desc_sw128(a_addr + kk * 32, 16, 1024);
+            const uint64_t bdesc = B_MN ? umma_desc_sw128(b_addr + kk * 2048, 8192, 1024)
+                                        : umma_desc_sw128(b_addr + kk * 32, 16, 1024);
+            tc2_mma_f16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          tc2_commit_mc(&empty[s], 0x3);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+        tc2_commit_mc(&tfull[acc], 0x3);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+  } else if (warp < C::EPI_WARPS) {
+    // =============== epilogue (both CTAs: own 128 rows x 256 columns) ===============
+    const int quad = warp & 3;
+    const int half = warp >> 2;
+    int acc = 0;
+    uint32_t aph = 0;
+    float* stage = epi_stage + warp * EPI_WARP_FLOATS;
+    for (int64_t t = cluster_id; t < total_tiles; t += n_clusters) {
+      int64_t z; int mt, nt;
+      tile_coords(t, tiles_m, tiles_n, group_m, z, mt, nt);
+      const int64_t m0 = static_cast<int64_t>(mt) * 256 + rank * 128, n0 = static_cast<int64_t>(nt) * H2_BN;
+      Epi epi;
+      epi.alpha = inst_alpha(p, z);
+      epi.beta = inst_beta(p, z);
+      epi.skip_ab = (epi.alpha == 0.0f);
+      const int64_t row0 = m0 + quad * 32;
+      const int rows_valid = static_cast<int>(min64(32, p.m - row0));
+      __half* Cz = static_cast<__half*>(p.c) + inst_off(p.c_off, p.stride_c, p.c_offs, z);
+      const int n_left = static_cast<int>(min64(H2_BN, p.n - n0));
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(acc * H2_BN);
+#pragma unroll 1
+      for (int cb = half * (H2_BN / 64); cb < (half + 1) * (H2_BN / 64); ++cb) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_row + cb * 32, v);
+        tmem_ld_wait();
+        if (rows_valid > 0 && cb * 32 < n_left)
+          epi_store_block(stage, v, Cz + (n0 + cb * 32) * p.ldc + row0, p.ldc, rows_valid, n_left - cb * 32, epi, lane);
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(&tempty[acc], 0);
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == C::MMA_WARP) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS)
+                 : "memory");
+  }
+}
+
+}  // namespace tb

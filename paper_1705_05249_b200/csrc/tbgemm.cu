@@ -21,6 +21,7 @@
 
 #include "hgemm_tc.cuh"
 #include "hgemm_tc_small.cuh"
+#include "hgemm_tc_2sm.cuh"
 #include "sgemm_simt.cuh"
 #include "sgemm_small.cuh"
 #include "tbgemm.h"
@@ -300,7 +301,8 @@ int launch_hg(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
   const int sms = sm_count() > 0 ? sm_count() : 148;
   const int64_t g = total < sms ? total : sms;
   dim3 grid(static_cast<unsigned>(g)), block(Cfg::THREADS);
-  const int group_m = 16;
+  int group_m = 16;
+  if (const char* gm = getenv("TBGEMM_GROUP_M")) group_m = atoi(gm);
   kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, group_m, total);
   char name[64];
   snprintf(name, sizeof(name), "hgemm_tc_%s_128x%d_%c%c%s", TMA ? "tma" : "ldg", BN, AMN ? 'm' : 'k',
@@ -316,6 +318,34 @@ int launch_hg_layout(const Call& c, const CUtensorMap& ta, const CUtensorMap& tb
   if (!amn && bmn) return launch_hg<BN, TMA, false, true, VEC>(c, ta, tbm);
   if (amn && !bmn) return launch_hg<BN, TMA, true, false, VEC>(c, ta, tbm);
   return launch_hg<BN, TMA, true, true, VEC>(c, ta, tbm);
+}
+
+template <bool AMN, bool BMN>
+int launch_h2(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
+  const Problem& p = c.p;
+  const int tiles_m = static_cast<int>((p.m + 255) / 256);
+  const int tiles_n = static_cast<int>((p.n + H2_BN - 1) / H2_BN);
+  const int64_t total = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
+  auto kern = hgemm_tc_2sm_kernel<AMN, BMN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, H2Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) {
+      set_err("cudaFuncSetAttribute", e);
+      return TB_ERR_CUDA;
+    }
+    attr_set = true;
+  }
+  const int sms = sm_count() > 0 ? sm_count() : 148;
+  const int64_t clusters = total < sms / 2 ? total : sms / 2;
+  dim3 grid(static_cast<unsigned>(2 * clusters)), block(H2Cfg::THREADS);
+  int group_m = 8;
+  if (const char* g = getenv("TBGEMM_GROUP_M")) group_m = atoi(g);
+  kern<<<grid, block, H2Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, group_m, total);
+  char name[64];
+  snprintf(name, sizeof(name), "hgemm_tc2sm_tma_256x256_%c%c", AMN ? 'm' : 'k', BMN ? 'n' : 'k');
+  record(name, grid, block, 2, H2Cfg::SMEM_BYTES, total);
+  return check_launch("hgemm_tc_2sm launch");
 }
 
 template <int BN>
@@ -335,9 +365,26 @@ int dispatch_hgemm_bn(const Call& c) {
     if (!amn) rc = make_map(&ta, A, p.k, p.m, p.batch, p.lda, p.stride_a, 64, 128);
     else rc = make_map(&ta, A, p.m, p.k, p.batch, p.lda, p.stride_a, 64, 64);
     if (rc != TB_OK) return rc;
-    if (!bmn) rc = make_map(&tbm, B, p.k, p.n, p.batch, p.ldb, p.stride_b, 64, BN);
+    // CTA-pair kernel for large problems (>= one wave of 256x256 pair tiles).
+    const int sms = sm_count() > 0 ? sm_count() : 148;
+    const int64_t pair_tiles = ((p.m + 255) / 256) * ((p.n + 255) / 256) * p.batch;
+    // Measured crossover (tools/exp9.py): the pair kernel keeps the tensor pipe
+    // ~97% busy vs ~87% up to ~5 TFLOP per call, but for the largest calls
+    // (16384^3, 32768^3) its L2 reuse collapses (329 GB DRAM reads at 32768^3
+    // vs 69 GB single-CTA), so those stay on the 128x256 single-CTA kernel.
+    const double flop = 2.0 * static_cast<double>(p.m) * p.n * p.k * p.batch;
+    const bool two_sm = BN == 256 && !(c.flags & TB_FLAG_NO_2SM) && pair_tiles >= sms / 2 && flop <= 6e12 &&
+                        !getenv("TBGEMM_NO_2SM");
+    const uint32_t bbox = two_sm ? 128 : BN;
+    if (!bmn) rc = make_map(&tbm, B, p.k, p.n, p.batch, p.ldb, p.stride_b, 64, bbox);
     else rc = make_map(&tbm, B, p.n, p.k, p.batch, p.ldb, p.stride_b, 64, 64);
     if (rc != TB_OK) return rc;
+    if (two_sm) {
+      if (!amn && !bmn) return launch_h2<false, false>(c, ta, tbm);
+      if (!amn && bmn) return launch_h2<false, true>(c, ta, tbm);
+      if (amn && !bmn) return launch_h2<true, false>(c, ta, tbm);
+      return launch_h2<true, true>(c, ta, tbm);
+    }
     return launch_hg_layout<BN, true, true>(c, ta, tbm);
   }
   if (al) return launch_hg_layout<BN, false, true>(c, ta, tbm);
