@@ -311,3 +311,48 @@ def test_large_sampled_parity(ctx, prec):
         orc.seqk_gemm("S", True, False, False, len(rows), len(cols), N, 1.0, Ar, 0, N, Br, 0,
                       len(cols), 0.0, sub, 0, len(cols))
         assert sub.reshape(len(rows), len(cols)).tobytes() == np.ascontiguousarray(got).tobytes()
+
+
+@pytest.mark.parametrize("layout", ["col", "row"])
+@pytest.mark.parametrize("ta", ["n", "t"])
+@pytest.mark.parametrize("tbn", ["n", "t"])
+def test_cta_pair_kernel_bitwise_equals_single_cta(ctx, layout, ta, tbn):
+    """The 2-SM (tcgen05 cta_group::2) kernel agrees bitwise with the
+    single-CTA kernel, and both with the float64 product within tolerance."""
+    import torch
+
+    from paper_1705_05249_b200.kernels import native
+    from paper_1705_05249_b200.kernels.dispatch import gemm_native
+
+    m, n, k = 4096, 4352, 576
+    prec = Precision.H
+    g = torch.Generator(device="cuda").manual_seed(3)
+    at = (torch.rand(m * k, device="cuda", generator=g) * 2 - 1).half()
+    bt = (torch.rand(k * n, device="cuda", generator=g) * 2 - 1).half()
+    a, b = tb.buffer_from_tensor(ctx, prec, at), tb.buffer_from_tensor(ctx, prec, bt)
+    a_rows, a_cols = (m, k) if ta == "n" else (k, m)
+    b_rows, b_cols = (k, n) if tbn == "n" else (n, k)
+    lda = a_rows if layout == "col" else a_cols
+    ldb = b_rows if layout == "col" else b_cols
+    ldc = m if layout == "col" else n
+    cfg = tb.routines.common.get_store(ctx).resolve("gemm", prec, ctx.device, (m, n, k))[0]
+    outs, kernels = [], []
+    for flags in (0, native.FLAG_NO_2SM):
+        c = tb.buffer_alloc(ctx, prec, m * n)
+        rec = gemm_native(ctx, prec, L[layout], T[ta], T[tbn], m, n, k, 1.0, a, 0, lda, b, 0, ldb, 0.0,
+                          c, 0, ldc, cfg, flags)
+        outs.append(c.device_tensor().clone())
+        kernels.append(rec["kernel"])
+    assert "2sm" in kernels[0] and "2sm" not in kernels[1], kernels
+    assert torch.equal(outs[0], outs[1]), kernels
+    # sampled rows against the float64 product
+    A = at.view(a_rows, a_cols).double() if layout == "row" else at.view(a_cols, a_rows).t().double()
+    B = bt.view(b_rows, b_cols).double() if layout == "row" else bt.view(b_cols, b_rows).t().double()
+    A = A if ta == "n" else A.t()
+    B = B if tbn == "n" else B.t()
+    rows = torch.arange(0, m, 257, device="cuda")
+    want = A[rows] @ B
+    C = outs[0].view(m, n) if layout == "row" else outs[0].view(n, m).t()
+    tol = 4 * 2.0 ** -10 * k * A[rows].abs().amax(1, keepdim=True) * B.abs().amax(0, keepdim=True) \
+        + 2.0 ** -11 * want.abs()
+    assert bool(((C[rows].double() - want).abs() <= tol).all())
