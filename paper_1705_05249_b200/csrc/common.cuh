@@ -31,7 +31,6 @@ struct Problem {
   const float* alphas; const float* betas;
   int64_t batch;
   int a_kcontig, b_ncontig;
-  int dbg;  // experiment switches (0 in production)
 };
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }

@@ -157,10 +157,8 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
         mbar_wait(&empty[s], ph ^ 1);
         const int64_t k0 = static_cast<int64_t>(kb) * HG_BK;
         const int k_left = static_cast<int>(min64(HG_BK, p.k - k0));
-        if (!(p.dbg & 2)) {
         small_fill<128, MI, A_MN, VEC>(sA + s * C::A_BYTES, ia, A, p.lda, m, k0, k_left, tid);
         small_fill<BN, NI, B_MN, VEC>(sB + s * C::B_BYTES, ib, B, p.ldb, n, k0, k_left, tid);
-        }
         if (VEC) {
           cp_async_commit();
           if (it >= C::DEPTH - 1) {
@@ -202,7 +200,7 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
                                         : umma_desc_sw128(a_addr + kk * 32, 16, 1024);
             const uint64_t bdesc = B_MN ? umma_desc_sw128(b_addr + kk * 2048, 8192, 1024)
                                         : umma_desc_sw128(b_addr + kk * 32, 16, 1024);
-            if (!(p.dbg & 4)) tc_mma_f16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
+            tc_mma_f16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
           }
           tc_commit(&empty[s]);
         }
@@ -237,9 +235,9 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
         uint32_t v[32];
         tmem_ld_32x32b_x32(t_row + cb * 32, v);
         tmem_ld_wait();
-        if (rows_valid > 0 && cb * 32 < n && !(p.dbg & 1))
+        if (rows_valid > 0 && cb * 32 < n)
           epi_store_block(stage, v, Cz + static_cast<int64_t>(cb * 32) * p.ldc + row0, p.ldc, rows_valid,
-                          n - cb * 32, epi, lane);
+                           n - cb * 32, epi, lane);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);

@@ -301,8 +301,7 @@ int launch_hg(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
   const int sms = sm_count() > 0 ? sm_count() : 148;
   const int64_t g = total < sms ? total : sms;
   dim3 grid(static_cast<unsigned>(g)), block(Cfg::THREADS);
-  int group_m = 16;
-  if (const char* gm = getenv("TBGEMM_GROUP_M")) group_m = atoi(gm);
+  const int group_m = 16;
   kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, group_m, total);
   char name[64];
   snprintf(name, sizeof(name), "hgemm_tc_%s_128x%d_%c%c%s", TMA ? "tma" : "ldg", BN, AMN ? 'm' : 'k',
@@ -339,8 +338,7 @@ int launch_h2(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
   const int sms = sm_count() > 0 ? sm_count() : 148;
   const int64_t clusters = total < sms / 2 ? total : sms / 2;
   dim3 grid(static_cast<unsigned>(2 * clusters)), block(H2Cfg::THREADS);
-  int group_m = 8;
-  if (const char* g = getenv("TBGEMM_GROUP_M")) group_m = atoi(g);
+  const int group_m = 8;  // measured best for pair tiles (tools/exp7.py)
   kern<<<grid, block, H2Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, group_m, total);
   char name[64];
   snprintf(name, sizeof(name), "hgemm_tc2sm_tma_256x256_%c%c", AMN ? 'm' : 'k', BMN ? 'n' : 'k');
@@ -373,8 +371,7 @@ int dispatch_hgemm_bn(const Call& c) {
     // (16384^3, 32768^3) its L2 reuse collapses (329 GB DRAM reads at 32768^3
     // vs 69 GB single-CTA), so those stay on the 128x256 single-CTA kernel.
     const double flop = 2.0 * static_cast<double>(p.m) * p.n * p.k * p.batch;
-    const bool two_sm = BN == 256 && !(c.flags & TB_FLAG_NO_2SM) && pair_tiles >= sms / 2 && flop <= 6e12 &&
-                        !getenv("TBGEMM_NO_2SM");
+    const bool two_sm = BN == 256 && !(c.flags & TB_FLAG_NO_2SM) && pair_tiles >= sms / 2 && flop <= 6e12;
     const uint32_t bbox = two_sm ? 128 : BN;
     if (!bmn) rc = make_map(&tbm, B, p.k, p.n, p.batch, p.ldb, p.stride_b, 64, bbox);
     else rc = make_map(&tbm, B, p.n, p.k, p.batch, p.ldb, p.stride_b, 64, 64);
@@ -500,8 +497,6 @@ Call make_call(int prec, int layout, int ta, int tbt, int64_t m, int64_t n, int6
   c.flags = flags;
   c.stream = static_cast<cudaStream_t>(stream);
   c.p.batch = 1;
-  const char* dbg = getenv("TBGEMM_DBG");
-  c.p.dbg = dbg ? atoi(dbg) : 0;
   return c;
 }
 
