@@ -56,14 +56,15 @@ enum {
   TB_OK = 0,
   TB_ERR_INVALID = 1,      /* argument rejected by the library */
   TB_ERR_CUDA = 2,         /* CUDA runtime / launch failure */
-  TB_ERR_UNSUPPORTED = 3,  /* e.g. no sm_100a device, TF32 flag on H */
+  TB_ERR_UNSUPPORTED = 3,  /* e.g. TF32 flag on H, or on unsupported operand layout */
   TB_ERR_DRIVER = 4        /* cuTensorMapEncodeTiled unavailable/failed */
 };
 
 /* Flags (bitwise OR). */
 enum {
   TB_FLAG_NONE = 0,
-  TB_FLAG_TF32 = 1,        /* opt-in TF32 tensor-core SGEMM (separate tolerance) */
+  TB_FLAG_TF32 = 1,        /* opt-in TF32 tensor-core SGEMM (separate tolerance;
+                              16-byte aligned, K-major operands) */
   TB_FLAG_NO_TMA = 2,      /* HGEMM: force the LDG producer (testing)          */
   TB_FLAG_SIMT_GENERAL = 4, /* SGEMM: force the general predicated kernel        */
   TB_FLAG_NO_PACK = 8,       /* HGEMM: no small-instance packing (testing)        */

@@ -22,6 +22,7 @@
 #include "hgemm_tc.cuh"
 #include "hgemm_tc_small.cuh"
 #include "hgemm_tc_2sm.cuh"
+#include "sgemm_tf32_tc.cuh"
 #include "sgemm_simt.cuh"
 #include "sgemm_small.cuh"
 #include "tbgemm.h"
@@ -92,21 +93,22 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-// 3-D FP16 tensor map: dims {contig, other, batch}, box {box0, box1, 1}, SW128.
+// 3-D tensor map (FP16 or FP32): dims {contig, other, batch}, box {box0, box1, 1}, SW128.
 int make_map(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t batch, uint64_t ld,
-             uint64_t stride, uint32_t box0, uint32_t box1) {
+             uint64_t stride, uint32_t box0, uint32_t box1,
+             CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT16, uint64_t es = 2) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) {
     snprintf(g_last_err, sizeof(g_last_err), "cuTensorMapEncodeTiled entry point unavailable");
     return TB_ERR_DRIVER;
   }
   cuuint64_t dims[3] = {d0, d1, batch};
-  uint64_t zstride = stride * 2;
-  if (batch <= 1) zstride = ((ld * d1 * 2) + 15) / 16 * 16;
-  cuuint64_t strides[2] = {ld * 2, zstride};
+  uint64_t zstride = stride * es;
+  if (batch <= 1) zstride = ((ld * d1 * es) + 15) / 16 * 16;
+  cuuint64_t strides[2] = {ld * es, zstride};
   cuuint32_t box[3] = {box0, box1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+  CUresult r = fn(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -218,12 +220,88 @@ int launch_ss_layout(const Call& c) {
   return launch_ss<MI, NI, TM, TN, true, true>(c);
 }
 
-int dispatch_sgemm(const Call& c) {
+template <int BN, bool AMN, bool BMN>
+int launch_tf32(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
+  using Cfg = TfCfg<BN>;
   const Problem& p = c.p;
-  if (c.flags & TB_FLAG_TF32) {
-    snprintf(g_last_err, sizeof(g_last_err), "TF32 SGEMM variant not built in this version");
+  const int tiles_m = static_cast<int>((p.m + HG_BM - 1) / HG_BM);
+  const int tiles_n = static_cast<int>((p.n + BN - 1) / BN);
+  const int64_t total = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
+  auto kern = sgemm_tf32_tc_kernel<BN, AMN, BMN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) {
+      set_err("cudaFuncSetAttribute", e);
+      return TB_ERR_CUDA;
+    }
+    attr_set = true;
+  }
+  const int sms = sm_count() > 0 ? sm_count() : 148;
+  const int64_t g = total < sms ? total : sms;
+  dim3 grid(static_cast<unsigned>(g)), block(Cfg::THREADS);
+  kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, 16, total);
+  char name[64];
+  snprintf(name, sizeof(name), "sgemm_tf32_tc_tma_128x%d_%c%c", BN, AMN ? 'm' : 'k', BMN ? 'n' : 'k');
+  record(name, grid, block, 1, Cfg::SMEM_BYTES, total);
+  return check_launch("sgemm_tf32_tc launch");
+}
+
+template <int BN>
+int dispatch_tf32_bn(const Call& c) {
+  const Problem& p = c.p;
+  const bool amn = !p.a_kcontig, bmn = p.b_ncontig;
+  const float* A = static_cast<const float*>(p.a) + p.a_off;
+  const float* B = static_cast<const float*>(p.b) + p.b_off;
+  CUtensorMap ta, tbm;
+  memset(&ta, 0, sizeof(ta));
+  memset(&tbm, 0, sizeof(tbm));
+  const CUtensorMapDataType F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  int rc = !amn ? make_map(&ta, A, p.k, p.m, p.batch, p.lda, p.stride_a, 32, 128, F32, 4)
+                : make_map(&ta, A, p.m, p.k, p.batch, p.lda, p.stride_a, 32, 32, F32, 4);
+  if (rc != TB_OK) return rc;
+  rc = !bmn ? make_map(&tbm, B, p.k, p.n, p.batch, p.ldb, p.stride_b, 32, BN, F32, 4)
+            : make_map(&tbm, B, p.n, p.k, p.batch, p.ldb, p.stride_b, 32, 32, F32, 4);
+  if (rc != TB_OK) return rc;
+  if (!amn && !bmn) return launch_tf32<BN, false, false>(c, ta, tbm);
+  if (!amn && bmn) return launch_tf32<BN, false, true>(c, ta, tbm);
+  if (amn && !bmn) return launch_tf32<BN, true, false>(c, ta, tbm);
+  return launch_tf32<BN, true, true>(c, ta, tbm);
+}
+
+// Opt-in TF32 tensor-core SGEMM (TB_FLAG_TF32): TMA producer only, so the
+// operands must be 16-byte aligned with arithmetic batch offsets.
+int dispatch_tf32(const Call& c) {
+  const Problem& p = c.p;
+  bool ok = (p.lda % 4 == 0) && (p.ldb % 4 == 0) && aligned_elems(p.a, p.a_off, 4, 16) &&
+            aligned_elems(p.b, p.b_off, 4, 16) && !p.a_offs && !p.b_offs;
+  if (p.batch > 1) ok = ok && (p.stride_a % 4 == 0) && (p.stride_b % 4 == 0);
+  if (!ok) {
+    snprintf(g_last_err, sizeof(g_last_err),
+             "TF32 path needs 16-byte aligned operands (ld and offsets multiples of 4) and strided batches");
     return TB_ERR_UNSUPPORTED;
   }
+  // UMMA reads MN-major 32-bit operands only in the SWIZZLE_128B_BASE32B
+  // canonical layout, which this version does not build: K-major operands
+  // only (col-major T x N, row-major N x T).
+  if (!p.a_kcontig || p.b_ncontig) {
+    snprintf(g_last_err, sizeof(g_last_err),
+             "TF32 path supports K-major operands only (col-major trans_a=T,trans_b=N / row-major N,T)");
+    return TB_ERR_UNSUPPORTED;
+  }
+  const int sms = sm_count() > 0 ? sm_count() : 148;
+  int bn = 256;
+  auto tiles = [&](int b) { return ((p.m + HG_BM - 1) / HG_BM) * ((p.n + b - 1) / b) * p.batch; };
+  while (bn > 64 && tiles(bn) < sms) bn /= 2;
+  if (bn == 256) return dispatch_tf32_bn<256>(c);
+  if (bn == 128) return dispatch_tf32_bn<128>(c);
+  return dispatch_tf32_bn<64>(c);
+}
+
+int dispatch_sgemm(const Call& c) {
+  const Problem& p = c.p;
+  // k == 0 / alpha == 0 need no products: the FFMA kernels' epilogue handles them.
+  if ((c.flags & TB_FLAG_TF32) && p.k > 0 && !(p.alphas == nullptr && p.alpha == 0.0f)) return dispatch_tf32(c);
   // 16-byte vector loads need every operand element base and ld to be
   // multiples of 4 floats.
   bool vec = (p.lda % 4 == 0) && (p.ldb % 4 == 0) && aligned_elems(p.a, 0, 4, 16) && aligned_elems(p.b, 0, 4, 16);

@@ -21,8 +21,9 @@ from __future__ import annotations
 
 import numpy as np
 
-from ..core import Buffer, Context, Layout, Transpose, matrix_span
+from ..core import Buffer, Context, Layout, Precision, Transpose, matrix_span
 from ..errors import UsageError
+from ..kernels import native
 from ..kernels.dispatch import gemm_batched_native, gemm_strided_batched_native, prec_code
 from ..kernels.engine import WorkGrid, pre_launch, record_launch, reference_grid
 from .common import check_precision, get_store, scalars, stored_dims
@@ -161,8 +162,9 @@ def gemm_strided_batched(ctx: Context, layout: Layout, trans_a: Transpose, trans
                          stride_b: int, beta, c: Buffer, stride_c: int, batch_count: int, *,
                          a_offset: int = 0, b_offset: int = 0, c_offset: int = 0,
                          lda: int | None = None, ldb: int | None = None,
-                         ldc: int | None = None) -> None:
-    """Instance i uses base offset + i*stride per matrix (extras.py:309-348)."""
+                         ldc: int | None = None, tf32: bool = False) -> None:
+    """Instance i uses base offset + i*stride per matrix (extras.py:309-348).
+    ``tf32=True`` opts in to the TF32 tensor-core kernel (see ``gemm``)."""
     if batch_count < 1:
         raise UsageError("batch_count must be >= 1")
     lda_e, ldb_e, ldc_e = _default_lds(layout, trans_a, trans_b, m, n, k, lda, ldb, ldc)
@@ -182,6 +184,8 @@ def gemm_strided_batched(ctx: Context, layout: Layout, trans_a: Transpose, trans
     lda_e, ldb_e, ldc_e, c_span = _validate(ctx, layout, trans_a, trans_b, m, n, k, a, a_offs, lda,
                                             b, b_offs, ldb, c, c_offs, ldc, batch_count)
     precision = a.precision
+    if tf32 and precision is not Precision.S:
+        raise UsageError("tf32 applies to Precision.S only")
     al = scalars([alpha], precision)[0]
     be = scalars([beta], precision)[0]
     # stride_c >= one instance extent was checked above, so strided outputs
@@ -197,6 +201,6 @@ def gemm_strided_batched(ctx: Context, layout: Layout, trans_a: Transpose, trans
     launched = gemm_strided_batched_native(
         ctx, precision, layout, trans_a, trans_b, m, n, k, float(al),
         a, a_offset, lda_e, stride_a, b, b_offset, ldb_e, stride_b, float(be),
-        c, c_offset, ldc_e, stride_c, batch_count, cfg)
+        c, c_offset, ldc_e, stride_c, batch_count, cfg, native.FLAG_TF32 if tf32 else 0)
     if computes:
         record_launch(ctx, family, cfg, grid, launched)

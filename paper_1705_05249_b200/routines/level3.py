@@ -42,12 +42,15 @@ def gemm(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Transpose,
          a_offset: int = 0, lda: int | None = None,
          b_offset: int = 0, ldb: int | None = None,
          c_offset: int = 0, ldc: int | None = None,
-         kernel: str | None = None) -> None:
+         kernel: str | None = None, tf32: bool = False) -> None:
     """C = alpha * op(A) op(B) + beta * C on the GPU (asynchronous on the
     context's stream; read results with ``buffer_read`` / ``Buffer.data``).
 
     ``kernel`` forces the 'direct' or 'indirect' route (reference testing
-    knob, level3.py:99,110-111).
+    knob, level3.py:99,110-111).  ``tf32=True`` (Precision.S only) opts in to
+    the TF32 tensor-core kernel: inputs are rounded to TF32, so results meet
+    the TF32 tolerance 4*2^-10*K*max|a||b| instead of the FP32 one, and
+    operands must be 16-byte aligned.
     """
     precision = a.precision
     check_precision(ctx, precision, a, b, c)
@@ -56,6 +59,8 @@ def gemm(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Transpose,
     if kernel not in (None, "direct", "indirect"):
         raise UsageError("kernel must be None, 'direct' or 'indirect'")
     prec_code(precision)  # H / S only on this path
+    if tf32 and precision is not Precision.S:
+        raise UsageError("tf32 applies to Precision.S only")
     if m == 0 or n == 0:
         return
     a_rows, a_cols = stored_dims(trans_a, m, k)
@@ -84,5 +89,5 @@ def gemm(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Transpose,
     pre_launch(ctx, family, cfg, grid, precision)
     launched = gemm_native(ctx, precision, layout, trans_a, trans_b, m, n, k, alpha,
                            a, a_offset, lda, b, b_offset, ldb, beta, c, c_offset, ldc,
-                           cfg, route_flags(kernel))
+                           cfg, route_flags(kernel) | (native.FLAG_TF32 if tf32 else 0))
     record_launch(ctx, family, cfg, grid, launched)
