@@ -129,19 +129,23 @@ __device__ __forceinline__ int epi_idx(int c, int r) { return c * 32 + (r ^ ((c 
 // scalars.  `cblk` points at C element (row 0, col 0) of the block; rows /
 // cols beyond rows_valid / cols_valid are not written.  The reference
 // epilogue (Epi) is applied in FP32 and rounded once to FP16.
-__device__ __forceinline__ void epi_store_block(float* stage, const uint32_t (&v)[32], __half* cblk,
+template <int NCOL>
+__device__ __forceinline__ void epi_store_block(float* stage, const uint32_t (&v)[NCOL], __half* cblk,
                                                 int64_t ldc, int rows_valid, int cols_valid,
                                                 const Epi& epi, int lane) {
+  static_assert(NCOL == 16 || NCOL == 32, "16 or 32 columns");
 #pragma unroll
-  for (int c = 0; c < 32; ++c) stage[epi_idx(c, lane)] = __uint_as_float(v[c]);
+  for (int c = 0; c < NCOL; ++c) stage[epi_idx(c, lane)] = __uint_as_float(v[c]);
   __syncwarp();
-  const int cl = lane & 7, rg = lane >> 3;
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(cblk) & 15) == 0) && ((ldc & 7) == 0);
   // 0: alpha == 0 (beta*C or 0), 1: beta == 0 (alpha*acc), 2: general
   const int mode = epi.skip_ab ? 0 : (epi.beta == 0.0f ? 1 : 2);
+  // NCOL columns x 4 groups of 8 rows; quarter-warps cover 8 distinct columns.
 #pragma unroll
-  for (int cgi = 0; cgi < 4; ++cgi) {
-    const int c = cgi * 8 + cl;
+  for (int it = 0; it < NCOL / 8; ++it) {
+    const int item = it * 32 + lane;
+    const int c = (NCOL == 32) ? (it * 8 + (lane & 7)) : (item & 15);
+    const int rg = (NCOL == 32) ? (lane >> 3) : (item >> 4);
     const float4 x0 = *reinterpret_cast<const float4*>(stage + epi_idx(c, rg * 8));
     const float4 x1 = *reinterpret_cast<const float4*>(stage + epi_idx(c, rg * 8 + 4));
     if (c < cols_valid && rg * 8 < rows_valid) {

@@ -229,15 +229,22 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                              static_cast<uint32_t>(acc * BN + slot * NI);
-      // NI = 64: each column half takes one 32-column chunk; NI = 32: half 0 only
-#pragma unroll
-      for (int cb = half; cb < NI / 32; cb += 2) {
+      // NI = 64: each column half takes one 32-column chunk; NI = 32: each
+      // half takes 16 columns (x16 TMEM loads).
+      if (NI == 64) {
         uint32_t v[32];
-        tmem_ld_32x32b_x32(t_row + cb * 32, v);
+        tmem_ld_32x32b_x32(t_row + half * 32, v);
         tmem_ld_wait();
-        if (rows_valid > 0 && cb * 32 < n)
-          epi_store_block(stage, v, Cz + static_cast<int64_t>(cb * 32) * p.ldc + row0, p.ldc, rows_valid,
-                           n - cb * 32, epi, lane);
+        if (rows_valid > 0 && half * 32 < n)
+          epi_store_block<32>(stage, v, Cz + static_cast<int64_t>(half * 32) * p.ldc + row0, p.ldc, rows_valid,
+                              n - half * 32, epi, lane);
+      } else {
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(t_row + half * 16, v);
+        tmem_ld_wait();
+        if (rows_valid > 0 && half * 16 < n)
+          epi_store_block<16>(stage, v, Cz + static_cast<int64_t>(half * 16) * p.ldc + row0, p.ldc, rows_valid,
+                              n - half * 16, epi, lane);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
