@@ -295,6 +295,15 @@ def run_ours(args, rank, world, local_rank):
                 extra[name] = {"error": repr(exc)}
             torch.cuda.empty_cache()
 
+    # North star: batched small-matrix GEMM >= 10x the naive per-matrix launch
+    # loop.  Loop = one public `gemm` call per instance (first 1024 instances
+    # of the 16384 x 32^3 batch, device-timed), extrapolated per instance.
+    if not args.no_extra:
+        try:
+            extra["batched_vs_loop"] = batched_vs_loop(tb, ctx, stream, torch)
+        except Exception as exc:  # noqa: BLE001
+            extra["batched_vs_loop"] = {"error": repr(exc)}
+
     if rank != 0:
         return None
     traffic = load_traffic(main["kernel"])
@@ -330,6 +339,31 @@ def run_ours(args, rank, world, local_rank):
     if extra:
         line["extra"] = extra
     return line
+
+
+def batched_vs_loop(tb, ctx, stream, torch, loop_instances: int = 1024) -> dict:
+    out = {}
+    for prec in (tb.Precision.H, tb.Precision.S):
+        w = WORKLOADS["batched_h32" if prec is tb.Precision.H else "batched_s32"]
+        _, a, b, c = make_operands(tb, ctx, w, 0, 1, torch)
+        s, e, batch = w["m"], w["m"] * w["m"], w["batch"]
+        L, T = tb.Layout.ROW_MAJOR, tb.Transpose.NO
+
+        def batched():
+            tb.gemm_strided_batched(ctx, L, T, T, s, s, s, 1.0, a, e, b, e, 0.0, c, e, batch)
+
+        def loop():
+            for i in range(loop_instances):
+                tb.gemm(ctx, L, T, T, s, s, s, 1.0, a, b, 0.0, c, a_offset=i * e, b_offset=i * e,
+                        c_offset=i * e)
+
+        t_b = sum(device_time(batched, 10, 3, stream, torch, lambda: None)) / 10
+        t_l = sum(device_time(loop, 2, 1, stream, torch, lambda: None)) / 2
+        per_inst_loop = t_l / loop_instances
+        out[prec.value] = {"batched_ms": round(t_b * 1e3, 4), "loop_ms_per_instance": round(per_inst_loop * 1e3, 5),
+                           "speedup": round(per_inst_loop * batch / t_b, 1),
+                           "workload": f"{batch} x {s}^3 strided batched vs {loop_instances} single gemm calls"}
+    return out
 
 
 def load_traffic(kernel: str):

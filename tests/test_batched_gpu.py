@@ -203,3 +203,40 @@ def test_small_path_bitwise_equals_general_path(ctx, prec, layout, ta, tbt, shap
     if small_expected:
         assert "small" in kernels[0], kernels
     assert outs[0].tobytes() == outs[1].tobytes(), kernels
+
+
+def test_batched_beats_looped_launches_10x(ctx):
+    """North star / acceptance criterion (test_acceptance.py:168-204 asks >= 1.2x
+    on the host): one batched launch vs one gemm call per instance, >= 10x."""
+    import time
+
+    import torch
+
+    rng = np.random.default_rng(3)
+    s, batch = 32, 512
+    e = s * s
+    host, (a, b, c), _ = setup(ctx, rng, s, s, s, batch, Precision.S)
+    c2 = tb.buffer_alloc(ctx, Precision.S, batch * e)
+
+    def batched():
+        tb.gemm_strided_batched(ctx, COL, NO, NO, s, s, s, 1.0, a, e, b, e, 0.0, c, e, batch)
+
+    def looped():
+        for i in range(batch):
+            tb.gemm(ctx, COL, NO, NO, s, s, s, 1.0, a, b, 0.0, c2, a_offset=i * e, b_offset=i * e,
+                    c_offset=i * e)
+
+    def best(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        out = float("inf")
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            out = min(out, time.perf_counter() - t0)
+        return out
+
+    speedup = best(looped) / best(batched)
+    assert tb.buffer_read(c, 0, batch * e).tobytes() == tb.buffer_read(c2, 0, batch * e).tobytes()
+    assert speedup >= 10.0, speedup
