@@ -249,26 +249,65 @@ def run_ours(args, rank, world, local_rank):
     w = main["w"]
 
     # ---- e2e: public API with host buffers, copies inside the timed region ----
+    # Every step copies its A and B from pinned host memory, runs the routine
+    # and copies C back.  Steps are software-pipelined over three streams
+    # (H2D copy engine, compute, D2H copy engine) with double-buffered device
+    # operands, so step i's D2H and step i+1's H2D overlap (PCIe is full
+    # duplex) — the copies of every step stay inside the timed region.
     prec, a, b, c = main["prec"], main["a"], main["b"], main["c"]
-    host_a = torch.empty(a.length, dtype=prec.torch_dtype, pin_memory=True)
-    host_b = torch.empty(b.length, dtype=prec.torch_dtype, pin_memory=True)
-    host_c = torch.empty(c.length, dtype=prec.torch_dtype, pin_memory=True)
+    dt = prec.torch_dtype
+    host_a = torch.empty(a.length, dtype=dt, pin_memory=True)
+    host_b = torch.empty(b.length, dtype=dt, pin_memory=True)
+    host_c = [torch.empty(c.length, dtype=dt, pin_memory=True) for _ in range(2)]
     host_a.copy_(a.device_tensor())
     host_b.copy_(b.device_tensor())
-    dev_a, dev_b, dev_c = a.device_tensor(), b.device_tensor(), c.device_tensor()
-    fn = main["fn"]
+    sets = [(a, b, c)]
+    sets.append(tuple(tb.buffer_from_tensor(ctx, prec, torch.empty(x.length, dtype=dt, device=dev))
+                      for x in (a, b, c)))
+    s_h2d, s_cmp, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    fns = [step_fn(tb, ctx, w, prec, *st) for st in sets]
 
-    def e2e_step():
-        dev_a.copy_(host_a, non_blocking=True)
-        dev_b.copy_(host_b, non_blocking=True)
-        fn()
-        host_c.copy_(dev_c, non_blocking=True)
+    def run_e2e(n_steps):
+        done_cmp = [None, None]   # compute finished with set i (its inputs are free)
+        done_d2h = [None, None]   # D2H finished with set i (its C is free)
+        for i in range(n_steps):
+            j = i & 1
+            da, db, dc = (x.device_tensor() for x in sets[j])
+            with torch.cuda.stream(s_h2d):
+                if done_cmp[j] is not None:
+                    s_h2d.wait_event(done_cmp[j])
+                da.copy_(host_a, non_blocking=True)
+                db.copy_(host_b, non_blocking=True)
+                ev_in = torch.cuda.Event()
+                ev_in.record(s_h2d)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(ev_in)
+                if done_d2h[j] is not None:
+                    s_cmp.wait_event(done_d2h[j])
+                fns[j]()
+                done_cmp[j] = torch.cuda.Event()
+                done_cmp[j].record(s_cmp)
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(done_cmp[j])
+                host_c[j].copy_(dc, non_blocking=True)
+                done_d2h[j] = torch.cuda.Event()
+                done_d2h[j].record(s_d2h)
 
-    e2e_steps = max(3, min(args.steps, 20))
+    e2e_steps = max(4, min(args.steps, 20))
+    run_e2e(2)
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    e2e_times = device_time(e2e_step, e2e_steps, max(1, args.warmup), stream, torch, lambda: None)
-    e2e_total = sum(e2e_times)
+    t0_ev, t1_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0_ev.record(s_h2d)
+    for st_ in (s_cmp, s_d2h):
+        st_.wait_event(t0_ev)
+    run_e2e(e2e_steps)
+    for st_ in (s_cmp, s_h2d):
+        s_d2h.wait_stream(st_)
+    t1_ev.record(s_d2h)
+    torch.cuda.synchronize()
+    e2e_total = t0_ev.elapsed_time(t1_ev) / 1e3
     if world > 1:
         t = torch.tensor([e2e_total], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -276,8 +315,9 @@ def run_ours(args, rank, world, local_rank):
     es = prec.elemsize
     e2e = {"value": round(flops(w) * world * e2e_steps / e2e_total / 1e9, 2), "unit": "GFLOPS",
            "h2d_bytes_per_step": (a.length + b.length) * es, "d2h_bytes_per_step": c.length * es,
-           "ms_per_step": round(e2e_total / e2e_steps * 1e3, 4),
-           "path": "pinned host A,B -> device; gemm (C-ABI via public API); device C -> pinned host"}
+           "ms_per_step": round(e2e_total / e2e_steps * 1e3, 4), "steps": e2e_steps,
+           "path": "pinned host A,B -> device (copy stream); public gemm API (compute stream); "
+                   "device C -> pinned host (copy stream); steps pipelined, double-buffered"}
 
     # ---- extras: the other headline configs (device-timed, this rank) ----
     extra = {}
