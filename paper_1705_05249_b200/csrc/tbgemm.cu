@@ -14,6 +14,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -60,6 +61,26 @@ int sm_count() {
     cached[dev] = v;
   }
   return cached[dev];
+}
+
+// The dynamic shared-memory opt-in is a per-device function attribute.
+struct SmemAttr {
+  std::atomic<uint64_t> devs{0};
+};
+
+template <typename K>
+int ensure_smem(SmemAttr& st, K kern, int bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (st.devs.load(std::memory_order_acquire) & bit) return TB_OK;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) {
+    set_err("cudaFuncSetAttribute", e);
+    return TB_ERR_CUDA;
+  }
+  st.devs.fetch_or(bit, std::memory_order_acq_rel);
+  return TB_OK;
 }
 
 int check_launch(const char* what) {
@@ -188,13 +209,10 @@ int launch_ss(const Call& c) {
   const Problem& p = c.p;
   const int64_t groups = (p.batch + Cfg::G - 1) / Cfg::G;
   auto kern = sgemm_small_kernel<MI, NI, TM, TN, AK, BNC>;
+  static SmemAttr attr;
+  if (int rc = ensure_smem(attr, kern, Cfg::SMEM_BYTES)) return rc;
   static int per_sm = 0;
   if (per_sm == 0) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    if (e != cudaSuccess) {
-      set_err("cudaFuncSetAttribute", e);
-      return TB_ERR_CUDA;
-    }
     int v = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, 256, Cfg::SMEM_BYTES) != cudaSuccess || v < 1) v = 1;
     per_sm = v;
@@ -228,15 +246,8 @@ int launch_tf32(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
   const int tiles_n = static_cast<int>((p.n + BN - 1) / BN);
   const int64_t total = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
   auto kern = sgemm_tf32_tc_kernel<BN, AMN, BMN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    if (e != cudaSuccess) {
-      set_err("cudaFuncSetAttribute", e);
-      return TB_ERR_CUDA;
-    }
-    attr_set = true;
-  }
+  static SmemAttr attr;  // per instantiation, per device
+  if (int rc = ensure_smem(attr, kern, Cfg::SMEM_BYTES)) return rc;
   const int sms = sm_count() > 0 ? sm_count() : 148;
   const int64_t g = total < sms ? total : sms;
   dim3 grid(static_cast<unsigned>(g)), block(Cfg::THREADS);
@@ -367,15 +378,8 @@ int launch_hg(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
   const int tiles_n = static_cast<int>((p.n + BN - 1) / BN);
   const int64_t total = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
   auto kern = hgemm_tc_kernel<BN, TMA, AMN, BMN, VEC>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    if (e != cudaSuccess) {
-      set_err("cudaFuncSetAttribute", e);
-      return TB_ERR_CUDA;
-    }
-    attr_set = true;
-  }
+  static SmemAttr attr;  // per instantiation, per device
+  if (int rc = ensure_smem(attr, kern, Cfg::SMEM_BYTES)) return rc;
   const int sms = sm_count() > 0 ? sm_count() : 148;
   const int64_t g = total < sms ? total : sms;
   dim3 grid(static_cast<unsigned>(g)), block(Cfg::THREADS);
@@ -404,15 +408,8 @@ int launch_h2(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
   const int tiles_n = static_cast<int>((p.n + H2_BN - 1) / H2_BN);
   const int64_t total = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
   auto kern = hgemm_tc_2sm_kernel<AMN, BMN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, H2Cfg::SMEM_BYTES);
-    if (e != cudaSuccess) {
-      set_err("cudaFuncSetAttribute", e);
-      return TB_ERR_CUDA;
-    }
-    attr_set = true;
-  }
+  static SmemAttr attr;  // per instantiation, per device
+  if (int rc = ensure_smem(attr, kern, H2Cfg::SMEM_BYTES)) return rc;
   const int sms = sm_count() > 0 ? sm_count() : 148;
   const int64_t clusters = total < sms / 2 ? total : sms / 2;
   dim3 grid(static_cast<unsigned>(2 * clusters)), block(H2Cfg::THREADS);
@@ -472,15 +469,8 @@ int launch_hs(const Call& c) {
   const Problem& p = c.p;
   const int64_t total = (p.batch + Cfg::P - 1) / Cfg::P;
   auto kern = hgemm_tc_small_kernel<MI, NI, AMN, BMN, VEC>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    if (e != cudaSuccess) {
-      set_err("cudaFuncSetAttribute", e);
-      return TB_ERR_CUDA;
-    }
-    attr_set = true;
-  }
+  static SmemAttr attr;  // per instantiation, per device
+  if (int rc = ensure_smem(attr, kern, Cfg::SMEM_BYTES)) return rc;
   const int sms = sm_count() > 0 ? sm_count() : 148;
   const int64_t g = total < sms ? total : sms;
   dim3 grid(static_cast<unsigned>(g)), block(Cfg::THREADS);

@@ -56,8 +56,18 @@ def _params(config: Configuration | None):
     return ctypes.byref(st)
 
 
+def _codes(layout: Layout, ta: Transpose, tb: Transpose) -> tuple:
+    """C-ABI enum codes (identity tests: cheaper than enum-keyed dicts)."""
+    lc = native.ROW_MAJOR if layout is Layout.ROW_MAJOR else native.COL_MAJOR
+    tac = native.NO_TRANS if ta is Transpose.NO else (
+        native.TRANS if ta is Transpose.YES else native.CONJ_TRANS)
+    tbc = native.NO_TRANS if tb is Transpose.NO else (
+        native.TRANS if tb is Transpose.YES else native.CONJ_TRANS)
+    return lc, tac, tbc
+
+
 def _stream(ctx: Context) -> int:
-    return ctx.stream.cuda_stream
+    return ctx.stream_handle()
 
 
 def gemm_native(ctx: Context, precision: Precision, layout: Layout, ta: Transpose, tb: Transpose,
@@ -68,7 +78,8 @@ def gemm_native(ctx: Context, precision: Precision, layout: Layout, ta: Transpos
     so = native.lib()
     pa, pb = a.data_ptr(), b.data_ptr()
     pc = c.data_ptr()
-    st = so.tb_gemm(prec_code(precision), _LAYOUT[layout], _TRANS[ta], _TRANS[tb],
+    lc, tac, tbc = _codes(layout, ta, tb)
+    st = so.tb_gemm(prec_code(precision), lc, tac, tbc,
                     m, n, k, float(alpha), pa, a_off, lda, pb, b_off, ldb, float(beta),
                     pc, c_off, ldc, _params(config), flags, _stream(ctx))
     c.mark_device_written()

@@ -12,6 +12,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+from collections.abc import Mapping
 from pathlib import Path
 
 from ..errors import TunedBlasError
@@ -162,7 +163,41 @@ def check(status: int, what: str) -> None:
             f"({so.tb_last_error().decode()})")
 
 
-def last_launch() -> dict:
+class NativeLaunch(Mapping):
+    """Read-only view of one ``tb_launch_record`` (copied at call time,
+    decoded to a dict on first access)."""
+
+    __slots__ = ("_rec", "_d")
+
+    def __init__(self, rec: TbLaunchRecord):
+        self._rec = rec
+        self._d = None
+
+    def _dict(self) -> dict:
+        d = self._d
+        if d is None:
+            d = self._d = self._rec.to_dict()
+        return d
+
+    def __getitem__(self, key):
+        return self._dict()[key]
+
+    def __iter__(self):
+        return iter(self._dict())
+
+    def __len__(self):
+        return len(self._dict())
+
+    def __eq__(self, other):
+        return dict(self._dict()) == (dict(other) if isinstance(other, Mapping) else other)
+
+    def __repr__(self):
+        return repr(self._dict())
+
+
+def last_launch() -> NativeLaunch:
     rec = TbLaunchRecord()
-    check(lib().tb_last_launch(ctypes.byref(rec)), "tb_last_launch")
-    return rec.to_dict()
+    st = lib().tb_last_launch(ctypes.byref(rec))
+    if st != TB_OK:
+        check(st, "tb_last_launch")
+    return NativeLaunch(rec)

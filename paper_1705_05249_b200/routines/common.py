@@ -35,8 +35,13 @@ def check_precision(ctx: Context, precision: Precision, *bufs: Buffer) -> None:
                 f"operand {i} has precision {buf.precision.value}, expected {precision.value}")
 
 
+_F32 = np.float32
+
+
 def scalar(value, precision: Precision):
     """Coerce a routine scalar to the compute dtype (common.py:68-76)."""
+    if (precision is Precision.S or precision is Precision.H) and type(value) in (float, int):
+        return _F32(value)
     if precision.is_complex:
         return precision.compute_dtype.type(complex(value))
     if isinstance(value, complex):
