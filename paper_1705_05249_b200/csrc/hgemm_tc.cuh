@@ -117,6 +117,42 @@ __device__ __forceinline__ void ldg_fill_tile(uint8_t* smem, const __half* base,
 }
 
 
+// K16 MMA steps in K block kb: 4, except in the last block, where steps that
+// would multiply only zero padding are not issued.  Every H kernel uses this
+// rule, so all H paths issue the same MMA sequence for an output element.
+__device__ __forceinline__ int hg_ksteps(int64_t k, int kb) {
+  const int64_t left = k - static_cast<int64_t>(kb) * HG_BK;
+  return left >= HG_BK ? HG_BK / 16 : static_cast<int>((left + 15) / 16);
+}
+
+struct Mma1Sm {
+  __device__ __forceinline__ void operator()(uint32_t d, uint64_t a, uint64_t b, uint32_t i, uint32_t acc) const {
+    tc_mma_f16(d, a, b, i, acc);
+  }
+};
+
+// Issue the K16 MMAs of one staged SWIZZLE_128B K block (A 128 rows / B BN
+// rows x 64 K).  Call from ALL lanes of the (converged) MMA warp: operands are
+// then warp-uniform and live in uniform registers, and one elected lane
+// issues.  A K16 step advances the descriptor's 14-bit start-address field by
+// 32 B (K-major) or 2048 B (MN-major).  `Mma` is tc_mma_f16 / tc2_mma_f16.
+template <bool A_MN, bool B_MN, typename Mma>
+__device__ __forceinline__ void hg_issue_kblock(Mma mma, uint32_t d_tmem, uint32_t a_addr, uint32_t b_addr,
+                                                uint32_t idesc, int ksteps, bool first_block) {
+  const uint64_t a0 = A_MN ? umma_desc_sw128(a_addr, 8192, 1024) : umma_desc_sw128(a_addr, 16, 1024);
+  const uint64_t b0 = B_MN ? umma_desc_sw128(b_addr, 8192, 1024) : umma_desc_sw128(b_addr, 16, 1024);
+  constexpr uint64_t ASTEP = A_MN ? 128 : 2, BSTEP = B_MN ? 128 : 2;
+  if (ksteps == HG_BK / 16) {
+#pragma unroll
+    for (int kk = 0; kk < HG_BK / 16; ++kk)
+      mma(d_tmem, a0 + ASTEP * kk, b0 + BSTEP * kk, idesc, (!first_block || kk != 0) ? 1u : 0u);
+  } else {
+#pragma unroll 1
+    for (int kk = 0; kk < ksteps; ++kk)
+      mma(d_tmem, a0 + ASTEP * kk, b0 + BSTEP * kk, idesc, (!first_block || kk != 0) ? 1u : 0u);
+  }
+}
+
 // Per-warp epilogue staging: 32 rows x 32 FP32 columns (4 KB).  Column c
 // holds row r at float index c*32 + (r ^ 4*(c%8)): conflict-free for the
 // row-per-lane writes and for the 8-rows-per-lane float4 reads below.
@@ -138,7 +174,10 @@ __device__ __forceinline__ void epi_store_block(float* stage, const uint32_t (&v
   for (int c = 0; c < NCOL; ++c) stage[epi_idx(c, lane)] = __uint_as_float(v[c]);
   __syncwarp();
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(cblk) & 15) == 0) && ((ldc & 7) == 0);
-  // 0: alpha == 0 (beta*C or 0), 1: beta == 0 (alpha*acc), 2: general
+  const bool full = vec_ok && rows_valid >= 32 && cols_valid >= NCOL;
+  // 0: alpha == 0 (beta*C or 0), 1: beta == 0 (alpha*acc), 2: general.  One
+  // runtime-mode body (measured: per-mode instantiations bloat the kernels
+  // and run slower).
   const int mode = epi.skip_ab ? 0 : (epi.beta == 0.0f ? 1 : 2);
   // NCOL columns x 4 groups of 8 rows; quarter-warps cover 8 distinct columns.
 #pragma unroll
@@ -148,10 +187,10 @@ __device__ __forceinline__ void epi_store_block(float* stage, const uint32_t (&v
     const int rg = (NCOL == 32) ? (lane >> 3) : (item >> 4);
     const float4 x0 = *reinterpret_cast<const float4*>(stage + epi_idx(c, rg * 8));
     const float4 x1 = *reinterpret_cast<const float4*>(stage + epi_idx(c, rg * 8 + 4));
-    if (c < cols_valid && rg * 8 < rows_valid) {
+    if (full || (c < cols_valid && rg * 8 < rows_valid)) {
       __half* dst = cblk + static_cast<int64_t>(c) * ldc + rg * 8;
       float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-      if (vec_ok && rg * 8 + 8 <= rows_valid) {
+      if (full || (vec_ok && rg * 8 + 8 <= rows_valid)) {
         if (mode == 1) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) x[i] = __fmul_rn(epi.alpha, x[i]);
@@ -196,7 +235,7 @@ __global__ void __launch_bounds__(HgCfg<BN, TMA>::THREADS, 1)
   using C = HgCfg<BN, TMA>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1024(smem_raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
@@ -291,35 +330,32 @@ __global__ void __launch_bounds__(HgCfg<BN, TMA>::THREADS, 1)
     }
   } else if (warp == C::MMA_WARP) {
     // ======================= MMA issuer =======================
-    if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_f16(HG_BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
-      int s = 0;
-      uint32_t ph = 0;
-      int acc = 0;
-      uint32_t aph = 0;
-      for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        mbar_wait(&tempty[acc], aph ^ 1);
+    // The whole warp runs the loop (uniform operands); one elected lane issues.
+    constexpr uint32_t idesc = umma_idesc_f16(HG_BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+    int s = 0;
+    uint32_t ph = 0;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[s], ph);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + s * C::A_BYTES);
-          const uint32_t b_addr = smem_u32(sB + s * C::B_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < HG_BK / 16; ++kk) {
-            const uint64_t adesc = A_MN ? umma_desc_sw128(a_addr + kk * 2048, 8192, 1024)
-                                        : umma_desc_sw128(a_addr + kk * 32, 16, 1024);
-            const uint64_t bdesc = B_MN ? umma_desc_sw128(b_addr + kk * 2048, 8192, 1024)
-                                        : umma_desc_sw128(b_addr + kk * 32, 16, 1024);
-            tc_mma_f16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
-          }
+        const uint32_t a_addr = smem_u32(sA + s * C::A_BYTES);
+        const uint32_t b_addr = smem_u32(sB + s * C::B_BYTES);
+        const int ksteps = hg_ksteps(p.k, kb);
+        if (elect_one()) {
+          hg_issue_kblock<A_MN, B_MN>(Mma1Sm{}, d_tmem, a_addr, b_addr, idesc, ksteps, kb == 0);
           tc_commit(&empty[s]);
-          if (++s == STAGES) { s = 0; ph ^= 1; }
         }
-        tc_commit(&tfull[acc]);
-        if (++acc == 2) { acc = 0; aph ^= 1; }
+        __syncwarp();
+        if (++s == STAGES) { s = 0; ph ^= 1; }
       }
+      if (elect_one()) tc_commit(&tfull[acc]);
+      __syncwarp();
+      if (++acc == 2) { acc = 0; aph ^= 1; }
     }
   } else if (warp < C::EPI_WARPS) {
     // ======================= epilogue =======================

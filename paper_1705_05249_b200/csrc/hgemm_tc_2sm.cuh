@@ -70,6 +70,11 @@ __device__ __forceinline__ void tc2_mma_f16(uint32_t d_tmem, uint64_t adesc, uin
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+struct Mma2Sm {
+  __device__ __forceinline__ void operator()(uint32_t d, uint64_t a, uint64_t b, uint32_t i, uint32_t acc) const {
+    tc2_mma_f16(d, a, b, i, acc);
+  }
+};
 __device__ __forceinline__ void tc2_commit_mc(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -93,7 +98,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
   using C = H2Cfg;
   constexpr int STAGES = H2_STAGES;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1024(smem_raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
@@ -172,7 +177,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
     }
   } else if (warp == C::MMA_WARP) {
     // =============== MMA issuer (leader CTA only) ===============
-    if (leader && lane == 0) {
+    // The whole warp runs the loop (uniform operands); one elected lane issues.
+    if (leader) {
       constexpr uint32_t idesc = umma_idesc_f16(256, H2_BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
       int s = 0;
       uint32_t ph = 0;
@@ -187,18 +193,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + s * C::A_BYTES);
           const uint32_t b_addr = smem_u32(sB + s * C::B_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < HG_BK / 16; ++kk) {
-            const uint64_t adesc = A_MN ? umma_desc_sw128(a_addr + kk * 2048, 8192, 1024)
-                                        : umma_desc_sw128(a_addr + kk * 32, 16, 1024);
-            const uint64_t bdesc = B_MN ? umma_desc_sw128(b_addr + kk * 2048, 8192, 1024)
-                                        : umma_desc_sw128(b_addr + kk * 32, 16, 1024);
-            tc2_mma_f16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
+          const int ksteps = hg_ksteps(p.k, kb);
+          if (elect_one()) {
+            hg_issue_kblock<A_MN, B_MN>(Mma2Sm{}, d_tmem, a_addr, b_addr, idesc, ksteps, kb == 0);
+            tc2_commit_mc(&empty[s], 0x3);
           }
-          tc2_commit_mc(&empty[s], 0x3);
+          __syncwarp();
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
-        tc2_commit_mc(&tfull[acc], 0x3);
+        if (elect_one()) tc2_commit_mc(&tfull[acc], 0x3);
+        __syncwarp();
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
     }

@@ -54,27 +54,32 @@ struct HsCfg {
 //   K-major : chunk j of thread t = row (t>>3) + 16j, K chunk t&7;
 //   MN-major: chunk j of thread t = sub-tile j/4, K row (t>>3) + 16(j%4),
 //             MN chunk t&7.
-// With that assignment every chunk's slot and smem offset is a compile-time
-// function of j plus a per-thread constant, so the loop body is a handful of
-// integer ops and one cp.async.
-template <int ROWS, int SLOT, bool MN, bool VEC>
+// K32 (k <= 32: the MMAs read K columns 0..31 only, see hg_ksteps): K-major
+// threads cover 4 chunks of a row, row (t>>2) + 32j, K chunk t&3; MN-major
+// skips the K rows >= 32.  Either way every chunk's slot and smem offset is a
+// compile-time function of j plus a per-thread constant, so the loop body is
+// a handful of integer ops and one cp.async, with no divergence.
+template <int ROWS, int SLOT, bool MN, bool VEC, bool K32>
 __device__ __forceinline__ void small_fill(uint8_t* smem, const __half* const (&inst)[4], const __half* any,
                                            int64_t ld, int extent, int64_t k0, int k_left, int tid) {
-  constexpr int PER_T = ROWS * 8 / 128;
-  const int q = tid >> 3;   // 0..15
-  const int c = tid & 7;    // 16-byte chunk within a 128-byte row
+  constexpr bool KM32 = K32 && !MN;
+  constexpr int PER_T = KM32 ? ROWS / 32 : ROWS * 8 / 128;
+  const int q = KM32 ? (tid >> 2) : (tid >> 3);  // 0..31 / 0..15
+  const int c = KM32 ? (tid & 3) : (tid & 7);    // 16-byte chunk within a 128-byte row
   const uint32_t off0 = static_cast<uint32_t>((q >> 3) * 1024 + (q & 7) * 128 + ((c ^ (q & 7)) << 4));
 #pragma unroll
   for (int j = 0; j < PER_T; ++j) {
+    if (K32 && MN && (j & 3) >= 2) continue;  // K rows 32..63: never read
     int slot, idx, valid;
     int64_t eoff;
     uint32_t off;
     if (!MN) {
-      slot = (16 * j) / SLOT;
-      idx = q + (16 * j) % SLOT;
+      constexpr int RSTEP = KM32 ? 32 : 16;
+      slot = (RSTEP * j) / SLOT;
+      idx = q + (RSTEP * j) % SLOT;
       valid = (idx < extent) ? min(8, k_left - c * 8) : 0;
       eoff = static_cast<int64_t>(idx) * ld + k0 + c * 8;
-      off = off0 + j * 2048;
+      off = off0 + j * (RSTEP * 128);
     } else {
       const int sub = j >> 2;
       const int mn = sub * 64 + c * 8;
@@ -97,13 +102,13 @@ __device__ __forceinline__ void small_fill(uint8_t* smem, const __half* const (&
   }
 }
 
-template <int MI, int NI, bool A_MN, bool B_MN, bool VEC>
+template <int MI, int NI, bool A_MN, bool B_MN, bool VEC, bool K32>
 __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
     hgemm_tc_small_kernel(Problem p, int64_t total_tiles) {
   using C = HsCfg<MI, NI>;
   constexpr int STAGES = C::STAGES, P = C::P, BN = C::BN, ACC = C::ACC;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1024(smem_raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
@@ -139,7 +144,10 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
     const int tid = threadIdx.x - C::PROD_WARP0 * 32;
     const __half* A = static_cast<const __half*>(p.a);
     const __half* B = static_cast<const __half*>(p.b);
-    int64_t it = 0;
+    int s = 0;
+    uint32_t ph = 0;
+    int lag = 0;  // stages committed but not yet published (<= DEPTH - 1)
+    int s_pub = 0;
     for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
       const int64_t zbase = t * P;
       const __half* ia[4];
@@ -152,69 +160,71 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
         ib[sl] = ok ? B + inst_off(p.b_off, p.stride_b, p.b_offs, zi) : nullptr;
       }
       for (int kb = 0; kb < nkb; ++kb) {
-        const int s = static_cast<int>(it % STAGES);
-        const uint32_t ph = static_cast<uint32_t>((it / STAGES) & 1);
         mbar_wait(&empty[s], ph ^ 1);
         const int64_t k0 = static_cast<int64_t>(kb) * HG_BK;
         const int k_left = static_cast<int>(min64(HG_BK, p.k - k0));
-        small_fill<128, MI, A_MN, VEC>(sA + s * C::A_BYTES, ia, A, p.lda, m, k0, k_left, tid);
-        small_fill<BN, NI, B_MN, VEC>(sB + s * C::B_BYTES, ib, B, p.ldb, n, k0, k_left, tid);
+        small_fill<128, MI, A_MN, VEC, K32>(sA + s * C::A_BYTES, ia, A, p.lda, m, k0, k_left, tid);
+        small_fill<BN, NI, B_MN, VEC, K32>(sB + s * C::B_BYTES, ib, B, p.ldb, n, k0, k_left, tid);
         if (VEC) {
           cp_async_commit();
-          if (it >= C::DEPTH - 1) {
+          if (lag == C::DEPTH - 1) {
             cp_async_wait<C::DEPTH - 1>();
             fence_proxy_async_smem();
-            mbar_arrive(&full[(it - (C::DEPTH - 1)) % STAGES]);
+            mbar_arrive(&full[s_pub]);
+            if (++s_pub == STAGES) s_pub = 0;
+          } else {
+            ++lag;
           }
         } else {
           fence_proxy_async_smem();
           mbar_arrive(&full[s]);
         }
-        ++it;
+        if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     }
     if (VEC) {
       cp_async_wait<0>();
       fence_proxy_async_smem();
-      for (int64_t j = (it > C::DEPTH - 1 ? it - (C::DEPTH - 1) : 0); j < it; ++j) mbar_arrive(&full[j % STAGES]);
+      for (; lag > 0; --lag) {
+        mbar_arrive(&full[s_pub]);
+        if (++s_pub == STAGES) s_pub = 0;
+      }
     }
   } else if (warp == C::MMA_WARP) {
     // ===================== MMA issuer =====================
-    if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_f16(128, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
-      int64_t it = 0, tile_i = 0;
-      for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tile_i) {
-        const int acc = static_cast<int>(tile_i % ACC);
-        mbar_wait(&tempty[acc], static_cast<uint32_t>(((tile_i / ACC) & 1) ^ 1));
+    // The whole warp runs the loop (uniform operands); one elected lane issues.
+    constexpr uint32_t idesc = umma_idesc_f16(128, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+    int s = 0, acc = 0;
+    uint32_t ph = 0, aph = 0;
+    for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[s], ph);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = static_cast<int>(it % STAGES);
-          mbar_wait(&full[s], static_cast<uint32_t>((it / STAGES) & 1));
-          tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + s * C::A_BYTES);
-          const uint32_t b_addr = smem_u32(sB + s * C::B_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < HG_BK / 16; ++kk) {
-            const uint64_t adesc = A_MN ? umma_desc_sw128(a_addr + kk * 2048, 8192, 1024)
-                                        : umma_desc_sw128(a_addr + kk * 32, 16, 1024);
-            const uint64_t bdesc = B_MN ? umma_desc_sw128(b_addr + kk * 2048, 8192, 1024)
-                                        : umma_desc_sw128(b_addr + kk * 32, 16, 1024);
-            tc_mma_f16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
-          }
+        const uint32_t a_addr = smem_u32(sA + s * C::A_BYTES);
+        const uint32_t b_addr = smem_u32(sB + s * C::B_BYTES);
+        const int ksteps = hg_ksteps(p.k, kb);
+        if (elect_one()) {
+          hg_issue_kblock<A_MN, B_MN>(Mma1Sm{}, d_tmem, a_addr, b_addr, idesc, ksteps, kb == 0);
           tc_commit(&empty[s]);
         }
-        tc_commit(&tfull[acc]);
+        __syncwarp();
+        if (++s == STAGES) { s = 0; ph ^= 1; }
       }
+      if (elect_one()) tc_commit(&tfull[acc]);
+      __syncwarp();
+      if (++acc == ACC) { acc = 0; aph ^= 1; }
     }
   } else if (warp < C::EPI_WARPS) {
     // ===================== epilogue =====================
     const int quad = warp & 3;
     const int half = warp >> 2;
     const int slot = (quad * 32) / MI;
-    int64_t tile_i = 0;
-    for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++tile_i) {
-      const int acc = static_cast<int>(tile_i % ACC);
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
       const int64_t zi = t * P + slot;
       const bool inst_ok = zi < p.batch;
       Epi epi;
@@ -225,7 +235,7 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
       const int row0 = quad * 32 - slot * MI;           // first instance row of this warp
       const int rows_valid = inst_ok ? min(32, m - row0) : 0;
       float* stage = epi_stage + warp * EPI_WARP_FLOATS;  // one buffer per epilogue warp
-      mbar_wait(&tfull[acc], static_cast<uint32_t>((tile_i / ACC) & 1));
+      mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                              static_cast<uint32_t>(acc * BN + slot * NI);
@@ -248,6 +258,7 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      if (++acc == ACC) { acc = 0; aph ^= 1; }
     }
   }
   tc_fence_before();

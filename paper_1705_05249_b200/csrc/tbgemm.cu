@@ -463,12 +463,12 @@ int dispatch_hgemm_bn(const Call& c) {
   return launch_hg_layout<BN, false, false>(c, ta, tbm);
 }
 
-template <int MI, int NI, bool AMN, bool BMN, bool VEC>
+template <int MI, int NI, bool AMN, bool BMN, bool VEC, bool K32>
 int launch_hs(const Call& c) {
   using Cfg = HsCfg<MI, NI>;
   const Problem& p = c.p;
   const int64_t total = (p.batch + Cfg::P - 1) / Cfg::P;
-  auto kern = hgemm_tc_small_kernel<MI, NI, AMN, BMN, VEC>;
+  auto kern = hgemm_tc_small_kernel<MI, NI, AMN, BMN, VEC, K32>;
   static SmemAttr attr;  // per instantiation, per device
   if (int rc = ensure_smem(attr, kern, Cfg::SMEM_BYTES)) return rc;
   const int sms = sm_count() > 0 ? sm_count() : 148;
@@ -476,26 +476,34 @@ int launch_hs(const Call& c) {
   dim3 grid(static_cast<unsigned>(g)), block(Cfg::THREADS);
   kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(p, total);
   char name[64];
-  snprintf(name, sizeof(name), "hgemm_tc_small_%dx%d_p%d_%c%c%s", MI, NI, Cfg::P, AMN ? 'm' : 'k',
-           BMN ? 'n' : 'k', VEC ? "_cpasync" : "_scalar");
+  snprintf(name, sizeof(name), "hgemm_tc_small_%dx%d_p%d_%c%c%s%s", MI, NI, Cfg::P, AMN ? 'm' : 'k',
+           BMN ? 'n' : 'k', VEC ? "_cpasync" : "_scalar", K32 ? "_k32" : "");
   record(name, grid, block, 1, Cfg::SMEM_BYTES, total);
   return check_launch("hgemm_tc_small launch");
 }
 
-template <int MI, int NI, bool VEC>
+template <int MI, int NI, bool VEC, bool K32>
 int launch_hs_layout(const Call& c) {
   const bool amn = !c.p.a_kcontig, bmn = c.p.b_ncontig;
-  if (!amn && !bmn) return launch_hs<MI, NI, false, false, VEC>(c);
-  if (!amn && bmn) return launch_hs<MI, NI, false, true, VEC>(c);
-  if (amn && !bmn) return launch_hs<MI, NI, true, false, VEC>(c);
-  return launch_hs<MI, NI, true, true, VEC>(c);
+  if (!amn && !bmn) return launch_hs<MI, NI, false, false, VEC, K32>(c);
+  if (!amn && bmn) return launch_hs<MI, NI, false, true, VEC, K32>(c);
+  if (amn && !bmn) return launch_hs<MI, NI, true, false, VEC, K32>(c);
+  return launch_hs<MI, NI, true, true, VEC, K32>(c);
 }
 
+template <bool VEC, bool K32>
+int dispatch_hsmall_k(const Call& c) {
+  const Problem& p = c.p;
+  if (p.m <= 32) return p.n <= 32 ? launch_hs_layout<32, 32, VEC, K32>(c) : launch_hs_layout<32, 64, VEC, K32>(c);
+  return p.n <= 32 ? launch_hs_layout<64, 32, VEC, K32>(c) : launch_hs_layout<64, 64, VEC, K32>(c);
+}
+
+// k <= 32 (one partial K block; the MMAs read K columns 0..31 only): the K32
+// fill skips the unread half of each staged row.  Same MMA sequence either way.
 template <bool VEC>
 int dispatch_hsmall(const Call& c) {
-  const Problem& p = c.p;
-  if (p.m <= 32) return p.n <= 32 ? launch_hs_layout<32, 32, VEC>(c) : launch_hs_layout<32, 64, VEC>(c);
-  return p.n <= 32 ? launch_hs_layout<64, 32, VEC>(c) : launch_hs_layout<64, 64, VEC>(c);
+  if (VEC && c.p.k <= 32) return dispatch_hsmall_k<VEC, true>(c);
+  return dispatch_hsmall_k<VEC, false>(c);
 }
 
 int dispatch_hgemm(const Call& c) {
