@@ -276,13 +276,14 @@ __global__ void __launch_bounds__(HgCfg<BN, TMA>::THREADS, 1)
     int s = 0;
     uint32_t ph = 0;
     if (TMA) {
-      if (lane == 0) {
-        for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-          int64_t z; int mt, nt;
-          tile_coords(t, tiles_m, tiles_n, group_m, z, mt, nt);
-          const int m0 = mt * HG_BM, n0 = nt * BN, zz = static_cast<int>(z);
-          for (int kb = 0; kb < nkb; ++kb) {
-            mbar_wait(&empty[s], ph ^ 1);
+      // The whole warp runs the loop (uniform coordinates); one elected lane issues.
+      for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        int64_t z; int mt, nt;
+        tile_coords(t, tiles_m, tiles_n, group_m, z, mt, nt);
+        const int m0 = mt * HG_BM, n0 = nt * BN, zz = static_cast<int>(z);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (elect_one()) {
             mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
             const int k0 = kb * HG_BK;
             uint8_t* a_dst = sA + s * C::A_BYTES;
@@ -299,8 +300,9 @@ __global__ void __launch_bounds__(HgCfg<BN, TMA>::THREADS, 1)
 #pragma unroll
               for (int c = 0; c < BN / 64; ++c) tma_load_3d(b_dst + c * 8192, &tmB, &full[s], n0 + c * 64, k0, zz);
             }
-            if (++s == STAGES) { s = 0; ph ^= 1; }
           }
+          __syncwarp();
+          if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
     } else {

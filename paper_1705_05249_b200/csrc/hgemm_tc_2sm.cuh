@@ -144,17 +144,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
 
   if (warp == C::PROD_WARP) {
     // =============== producer (both CTAs: own A half + own B half) ===============
-    if (lane == 0) {
-      int s = 0;
-      uint32_t ph = 0;
-      for (int64_t t = cluster_id; t < total_tiles; t += n_clusters) {
-        int64_t z; int mt, nt;
-        tile_coords(t, tiles_m, tiles_n, group_m, z, mt, nt);
-        const int m0 = mt * 256 + static_cast<int>(rank) * 128;
-        const int n0 = nt * H2_BN + static_cast<int>(rank) * (H2_BN / 2);
-        const int zz = static_cast<int>(z);
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
+    // The whole warp runs the loop (uniform coordinates); one elected lane issues.
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = cluster_id; t < total_tiles; t += n_clusters) {
+      int64_t z; int mt, nt;
+      tile_coords(t, tiles_m, tiles_n, group_m, z, mt, nt);
+      const int m0 = mt * 256 + static_cast<int>(rank) * 128;
+      const int n0 = nt * H2_BN + static_cast<int>(rank) * (H2_BN / 2);
+      const int zz = static_cast<int>(z);
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        if (elect_one()) {
           if (leader) mbar_arrive_expect_tx(&full[s], 2 * C::STAGE_BYTES);
           const int k0 = kb * HG_BK;
           uint8_t* a_dst = sA + s * C::A_BYTES;
@@ -171,8 +172,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
             tma_load_3d_2sm(b_dst, &tmB, &full[s], n0, k0, zz);
             tma_load_3d_2sm(b_dst + 8192, &tmB, &full[s], n0 + 64, k0, zz);
           }
-          if (++s == STAGES) { s = 0; ph ^= 1; }
         }
+        __syncwarp();
+        if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp == C::MMA_WARP) {
