@@ -35,10 +35,12 @@ struct SsCfg {
   // 3-4 stages, <= ~100 KB so two CTAs share an SM
   static constexpr int STAGES = (4 * STAGE_FLOATS * 4 <= 100 * 1024) ? 4 : 3;
   static constexpr int SMEM_BYTES = STAGES * STAGE_FLOATS * 4;
+  // 8x8 micro-tiles need > 128 registers: one CTA per SM
+  static constexpr int MINB = (TM * TN >= 64) ? 1 : 2;
 };
 
 template <int MI, int NI, int TM, int TN, bool AK, bool BNC>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, (SsCfg<MI, NI, TM, TN>::MINB))
     sgemm_small_kernel(Problem p, int64_t groups) {
   using C = SsCfg<MI, NI, TM, TN>;
   constexpr int QM = C::QM, QN = C::QN;
@@ -71,9 +73,7 @@ __global__ void __launch_bounds__(256, 2)
   // constant, so only the instance pointers are computed per stage.
   constexpr int A_CH = MI * KC / 4, B_CH = NI * KC / 4;
   static_assert(A_CH % 256 == 0 && B_CH % 256 == 0, "whole chunks per thread");
-  auto issue = [&](int64_t si, int s) {
-    const int64_t gi = blockIdx.x + (si / kchunks) * gridDim.x;
-    const int kc = static_cast<int>(si % kchunks);
+  auto issue = [&](int64_t gi, int kc, int s) {
     const int64_t k0 = static_cast<int64_t>(kc) * KC;
     const int k_left = static_cast<int>(min64(KC, p.k - k0));
     float* st = stage_ptr(s);
@@ -127,11 +127,28 @@ __global__ void __launch_bounds__(256, 2)
     }
   };
 
+  // Stage coordinates advance incrementally (no 64-bit division per stage):
+  // chunk kc of group gi, then chunk 0 of group gi + gridDim.x.
+  auto advance = [&](int64_t& gi, int& kc) {
+    if (++kc == kchunks) {
+      kc = 0;
+      gi += gridDim.x;
+    }
+  };
+  int64_t gi_i = blockIdx.x;  // next stage to issue
+  int kc_i = 0;
+
   // prologue: STAGES-1 stages in flight
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < total) issue(s, s);
+    if (s < total) {
+      issue(gi_i, kc_i, s);
+      advance(gi_i, kc_i);
+    }
     cp_async_commit();
   }
+  int s_i = STAGES - 1, s_c = 0;  // ring slots: next issue / current compute
+  int64_t gi = blockIdx.x;        // current compute stage
+  int kc = 0;
 
   float acc[TM][TN];
 #pragma unroll
@@ -143,13 +160,15 @@ __global__ void __launch_bounds__(256, 2)
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     // refill the slot consumed in the previous iteration
-    const int64_t nxt = si + STAGES - 1;
-    if (nxt < total) issue(nxt, static_cast<int>(nxt % STAGES));
+    if (si + STAGES - 1 < total) {
+      issue(gi_i, kc_i, s_i);
+      advance(gi_i, kc_i);
+    }
     cp_async_commit();
+    if (++s_i == STAGES) s_i = 0;
 
-    const int s = static_cast<int>(si % STAGES);
-    const int kc = static_cast<int>(si % kchunks);
-    const int64_t gi = blockIdx.x + (si / kchunks) * gridDim.x;
+    const int s = s_c;
+    if (++s_c == STAGES) s_c = 0;
     const int k_left = static_cast<int>(min64(KC, p.k - static_cast<int64_t>(kc) * KC));
     const float* as = stage_ptr(s) + slot * C::A_ELEMS;
     const float* bs = stage_ptr(s) + G * C::A_ELEMS + slot * C::B_ELEMS;
@@ -262,6 +281,7 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
         for (int c = 0; c < TN; ++c) acc[r][c] = 0.0f;
     }
+    advance(gi, kc);
   }
   cp_async_wait<0>();
 }

@@ -348,6 +348,9 @@ int dispatch_sgemm(const Call& c) {
     const int64_t tiles256 = ((p.m + 127) / 128) * ((p.n + 255) / 256) * p.batch;
     if (tiles256 >= 4 * sms) return launch_simt<128, 256, 8, 8, 16, true, 1>(c, "128x256");
     if (tiles128 >= sms) return launch_simt<128, 128, 16, 8, 8, true, 1>(c, "128");
+    // < 1 wave of 128x128 (e.g. 1024^3, BASELINE C1): 64x128 4x8 (measured
+    // 30.7 vs 27.8 TFLOP/s for 64x64 4x4 at 1024^3; tools/sgemm_variants.cu)
+    if (p.n >= 128 && tiles128 * 2 >= sms) return launch_simt<64, 128, 16, 4, 8, true, 2>(c, "64x128");
   }
   if (mwg >= 128 && nwg < 128 && tiles128 * 2 >= sms) return launch_simt<128, 64, 16, 8, 4, true, 2>(c, "128x64");
   if (mwg < 128 && nwg >= 128 && tiles128 * 2 >= sms) return launch_simt<64, 128, 16, 4, 8, true, 2>(c, "64x128");

@@ -12,7 +12,7 @@ for w in which:
     a = tb.buffer_from_tensor(ctx, prec, (torch.rand(B*d*d, device='cuda')*2-1).to(dt))
     b = tb.buffer_from_tensor(ctx, prec, (torch.rand(B*d*d, device='cuda')*2-1).to(dt))
     c = tb.buffer_alloc(ctx, prec, B*d*d)
-    for _ in range(2):
+    for _ in range(int(__import__("os").environ.get("REPS", "2"))):
         tb.gemm_strided_batched(ctx, tb.Layout.ROW_MAJOR, T.NO, T.NO, d, d, d, 1.0, a, d*d, b, d*d, 0.0, c, d*d, B)
     torch.cuda.synchronize()
     print(w, ctx.last_launch.native["kernel"], flush=True)

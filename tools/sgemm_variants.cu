@@ -41,6 +41,14 @@ int main(int argc, char** argv) {
   p.c = c;
   run<128, 256, 8, 8, 16, 1>(p, reps, cref, "128x256x8 8x16 minb1");
   run<128, 128, 16, 8, 8, 1>(p, reps, cref, "128x128x16 8x8 minb1");
-  run<64, 256, 16, 4, 16, 1>(p, reps, cref, "64x256x16 4x16 minb1");
+  run<64, 64, 16, 4, 4, 2>(p, reps, cref, "64x64x16 4x4 (256t)");
+  run<64, 64, 16, 4, 8, 2>(p, reps, cref, "64x64x16 4x8 (128t)");
+  run<64, 64, 16, 8, 4, 2>(p, reps, cref, "64x64x16 8x4 (128t)");
+  run<64, 64, 16, 8, 8, 2>(p, reps, cref, "64x64x16 8x8 (64t)");
+  run<64, 64, 32, 8, 8, 2>(p, reps, cref, "64x64x32 8x8 (64t)");
+  run<64, 128, 16, 4, 8, 2>(p, reps, cref, "64x128x16 4x8 (256t)");
+  run<128, 64, 16, 8, 4, 2>(p, reps, cref, "128x64x16 8x4 (256t)");
+  run<64, 128, 16, 8, 8, 2>(p, reps, cref, "64x128x16 8x8 (128t)");
+  run<32, 64, 16, 4, 8, 2>(p, reps, cref, "32x64x16 4x8 (64t)");
   return 0;
 }
