@@ -68,7 +68,9 @@ enum {
   TB_FLAG_NO_TMA = 2,      /* HGEMM: force the LDG producer (testing)          */
   TB_FLAG_SIMT_GENERAL = 4, /* SGEMM: force the general predicated kernel        */
   TB_FLAG_NO_PACK = 8,       /* HGEMM: no small-instance packing (testing)        */
-  TB_FLAG_NO_2SM = 16        /* HGEMM: no CTA-pair (cta_group::2) kernel (testing) */
+  TB_FLAG_NO_2SM = 16,       /* HGEMM: no CTA-pair (cta_group::2) kernel (testing) */
+  TB_FLAG_NO_SPLITK = 32     /* HGEMM: no cluster split-K (testing; results then
+                                differ from the default route within tolerance) */
 };
 
 /*

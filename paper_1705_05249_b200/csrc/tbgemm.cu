@@ -23,6 +23,7 @@
 #include "hgemm_tc.cuh"
 #include "hgemm_tc_small.cuh"
 #include "hgemm_tc_2sm.cuh"
+#include "hgemm_tc_splitk.cuh"
 #include "sgemm_tf32_tc.cuh"
 #include "sgemm_simt.cuh"
 #include "sgemm_small.cuh"
@@ -509,6 +510,103 @@ int dispatch_hsmall(const Call& c) {
   return dispatch_hsmall_k<VEC, false>(c);
 }
 
+// Split-K cluster size for H: a pure function of (m, n, k) and the SM count
+// (never of batch or flags, so every H path of one shape issues the same
+// per-element MMA / reduction sequence).  Doubles while the 128x128 tiles of
+// one instance still leave half the SMs idle and each CTA keeps >= 16 K blocks
+// (measured: 1024^3 with 8 K blocks per CTA was slower split than unsplit).
+int hgemm_split_ks(const Problem& p) {
+  const int sms = sm_count() > 0 ? sm_count() : 148;
+  const int64_t t1 = ((p.m + HG_BM - 1) / HG_BM) * ((p.n + SK_BN - 1) / SK_BN);
+  const int64_t nkb = (p.k + HG_BK - 1) / HG_BK;
+  int ks = 1;
+  while (ks < 8 && t1 * ks * 2 <= sms && nkb >= 32 * ks) ks *= 2;
+  return ks;
+}
+
+template <bool TMA, bool AMN, bool BMN, bool VEC>
+int launch_hsk(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm, int ks) {
+  using Cfg = SkCfg<TMA>;
+  const Problem& p = c.p;
+  const int tiles_m = static_cast<int>((p.m + HG_BM - 1) / HG_BM);
+  const int tiles_n = static_cast<int>((p.n + SK_BN - 1) / SK_BN);
+  const int64_t total = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
+  auto kern = hgemm_tc_splitk_kernel<TMA, AMN, BMN, VEC>;
+  static SmemAttr attr;
+  if (int rc = ensure_smem(attr, kern, Cfg::SMEM_BYTES)) return rc;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeClusterDimension;
+  la[0].val.clusterDim.x = static_cast<unsigned>(ks);
+  la[0].val.clusterDim.y = 1;
+  la[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = c.stream;
+  cfg.attrs = la;
+  cfg.numAttrs = 1;
+  // Co-resident clusters only (clusters are placed within a GPC): the
+  // persistent loop then covers every tile without a second wave.
+  static int max_clusters[9] = {0};
+  if (max_clusters[ks] == 0) {
+    int v = 0;
+    cfg.gridDim = dim3(static_cast<unsigned>(ks));
+    if (cudaOccupancyMaxActiveClusters(&v, kern, &cfg) != cudaSuccess || v < 1) {
+      cudaGetLastError();
+      const int sms = sm_count() > 0 ? sm_count() : 148;
+      v = sms / ks;
+    }
+    max_clusters[ks] = v;
+  }
+  const int64_t clusters = total < max_clusters[ks] ? total : max_clusters[ks];
+  cfg.gridDim = dim3(static_cast<unsigned>(clusters * ks));
+  const int group_m = 16;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tbm, p, tiles_m, tiles_n, group_m, total);
+  if (e != cudaSuccess) {
+    set_err("hgemm_tc_splitk launch", e);
+    return TB_ERR_CUDA;
+  }
+  char name[64];
+  snprintf(name, sizeof(name), "hgemm_tc_splitk%d_%s_128x128_%c%c%s", ks, TMA ? "tma" : "ldg", AMN ? 'm' : 'k',
+           BMN ? 'n' : 'k', (!TMA && !VEC) ? "_scalar" : "");
+  record(name, cfg.gridDim, cfg.blockDim, ks, Cfg::SMEM_BYTES, total);
+  return check_launch("hgemm_tc_splitk launch");
+}
+
+template <bool TMA, bool VEC>
+int launch_hsk_layout(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm, int ks) {
+  const bool amn = !c.p.a_kcontig, bmn = c.p.b_ncontig;
+  if (!amn && !bmn) return launch_hsk<TMA, false, false, VEC>(c, ta, tbm, ks);
+  if (!amn && bmn) return launch_hsk<TMA, false, true, VEC>(c, ta, tbm, ks);
+  if (amn && !bmn) return launch_hsk<TMA, true, false, VEC>(c, ta, tbm, ks);
+  return launch_hsk<TMA, true, true, VEC>(c, ta, tbm, ks);
+}
+
+int dispatch_hsplit(const Call& c, int ks) {
+  const Problem& p = c.p;
+  const bool amn = !p.a_kcontig, bmn = p.b_ncontig;
+  const bool al = hgemm_aligned(c);
+  const bool generic = (p.a_offs != nullptr) || (p.b_offs != nullptr);
+  const bool big = p.m < (1LL << 31) && p.n < (1LL << 31) && p.k < (1LL << 31) && p.batch < (1LL << 31);
+  CUtensorMap ta, tbm;
+  memset(&ta, 0, sizeof(ta));
+  memset(&tbm, 0, sizeof(tbm));
+  if (al && !generic && big && !(c.flags & TB_FLAG_NO_TMA)) {
+    const __half* A = static_cast<const __half*>(p.a) + p.a_off;
+    const __half* B = static_cast<const __half*>(p.b) + p.b_off;
+    int rc;
+    if (!amn) rc = make_map(&ta, A, p.k, p.m, p.batch, p.lda, p.stride_a, 64, 128);
+    else rc = make_map(&ta, A, p.m, p.k, p.batch, p.lda, p.stride_a, 64, 64);
+    if (rc != TB_OK) return rc;
+    if (!bmn) rc = make_map(&tbm, B, p.k, p.n, p.batch, p.ldb, p.stride_b, 64, SK_BN);
+    else rc = make_map(&tbm, B, p.n, p.k, p.batch, p.ldb, p.stride_b, 64, 64);
+    if (rc != TB_OK) return rc;
+    return launch_hsk_layout<true, true>(c, ta, tbm, ks);
+  }
+  if (al) return launch_hsk_layout<false, true>(c, ta, tbm, ks);
+  return launch_hsk_layout<false, false>(c, ta, tbm, ks);
+}
+
 int dispatch_hgemm(const Call& c) {
   // Small instances (m, n <= 64): packed tcgen05 kernel.  Bitwise identical to
   // the general kernel (same per-element K sequence), so this is a pure
@@ -521,6 +619,8 @@ int dispatch_hgemm(const Call& c) {
     snprintf(g_last_err, sizeof(g_last_err), "TF32 flag applies to SGEMM only");
     return TB_ERR_UNSUPPORTED;
   }
+  // Few output tiles and a long K: split K across a cluster (DSMEM reduction).
+  if (const int ks = hgemm_split_ks(c.p); ks > 1 && !(c.flags & TB_FLAG_NO_SPLITK)) return dispatch_hsplit(c, ks);
   // Parameter mapping: NWG picks the UMMA N extent.  Pure function of the
   // parameters (never of batch) so single and batched calls of one shape use
   // the same MMA sequence (bitwise batched == looped).

@@ -33,12 +33,13 @@ __all__ = [
     "FLAG_SIMT_GENERAL",
     "FLAG_NO_PACK",
     "FLAG_NO_2SM",
+    "FLAG_NO_SPLITK",
 ]
 
 PREC_H, PREC_S = 0, 1
 COL_MAJOR, ROW_MAJOR = 0, 1
 NO_TRANS, TRANS, CONJ_TRANS = 0, 1, 2
-FLAG_TF32, FLAG_NO_TMA, FLAG_SIMT_GENERAL, FLAG_NO_PACK, FLAG_NO_2SM = 1, 2, 4, 8, 16
+FLAG_TF32, FLAG_NO_TMA, FLAG_SIMT_GENERAL, FLAG_NO_PACK, FLAG_NO_2SM, FLAG_NO_SPLITK = 1, 2, 4, 8, 16, 32
 TB_OK = 0
 
 #: Every symbol include/tbgemm.h declares (checked by tests/test_native_abi.py).
