@@ -2,7 +2,8 @@
 """Driver benchmark: GEMM GFLOPS of the B200-native hot path.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload hgemm|sgemm|batched_h32|batched_s32|batched_h64|batched_s64]
+                    [--workload hgemm|sgemm|batched_h32|batched_s32|batched_h64|batched_s64|
+                                sgemm_c1|hgemm_c3|sgemm_c3]
                     [--no-extra] [--no-cpu-baseline]
 
 A "step" is one call of the hot path on one batch of synthetic input:
@@ -14,7 +15,7 @@ A "step" is one call of the hot path on one batch of synthetic input:
 
 value   = whole-job GFLOPS with inputs resident in HBM, CUDA-event timed per
           step on the launching stream (max over ranks), L2 flushed between
-          steps (a 256 MiB write) so no step reads a warm L2.
+          steps (256 MiB write + 256 MiB read) so no step reads a warm L2.
 e2e     = the same metric through the public API with HOST buffers: pinned
           host → device copy of A and B, the routine, device → host copy of C,
           all inside the timed region.
@@ -60,6 +61,11 @@ WORKLOADS = {
     "batched_s32": dict(kind="batched", prec="S", m=32, n=32, k=32, batch=16384),
     "batched_h64": dict(kind="batched", prec="H", m=64, n=64, k=64, batch=16384),
     "batched_s64": dict(kind="batched", prec="S", m=64, n=64, k=64, batch=16384),
+    # the other BASELINE shapes: C1 (the reference's canonical 1024^3 SGEMM)
+    # and C3 (the im2col'd DL layer (4096, 128, 9216))
+    "sgemm_c1": dict(kind="gemm", prec="S", m=1024, n=1024, k=1024, batch=1),
+    "hgemm_c3": dict(kind="gemm", prec="H", m=4096, n=128, k=9216, batch=1),
+    "sgemm_c3": dict(kind="gemm", prec="S", m=4096, n=128, k=9216, batch=1),
 }
 
 
@@ -201,8 +207,16 @@ def run_ours(args, rank, world, local_rank):
     ctx = tb.context_create(tb.host_device())
     ctx.device_index = local_rank
     stream = torch.cuda.current_stream(dev)
+    # L2 flush before every step: a 256 MiB write evicts the inputs (126 MB
+    # L2), then a 256 MiB read of a second buffer evicts the flush's dirty
+    # lines, so the timed kernel starts from a cold, clean L2 and does not pay
+    # for unrelated write-backs (tools/exp15.py: C3 34.9 -> 30.5 us).
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    flush = lambda: flush_buf.fill_(1)  # noqa: E731  (256 MiB > 126 MB L2)
+    clean_buf = torch.ones(256 << 20, dtype=torch.uint8, device=dev)
+
+    def flush():
+        flush_buf.fill_(1)
+        clean_buf.view(torch.int64).sum()
     peaks, peak_src = load_peaks()
 
     def measure(name, steps, warmup):
@@ -225,7 +239,14 @@ def run_ours(args, rank, world, local_rank):
             total = float(t.item())
         per_launch = total / steps
         gflops = flops(w) * world * steps / total / 1e9
-        if w["prec"] == "H" and w["kind"] == "gemm":
+        ai = flops(w) / alg_bytes(w)
+        ridge = (peaks["bf16_tflops"] if w["prec"] == "H" else FFMA_TFLOPS) * 1e12 / (peaks["hbm_gbs"] * 1e9)
+        if w["kind"] == "gemm" and ai < ridge:
+            bound = "hbm"
+            peak, unit, achieved = peaks["hbm_gbs"], "GB/s", alg_bytes(w) / per_launch / 1e9
+            peak_note = (f"HBM copy bandwidth ({peak_src}: MEASURED_PEAKS.json hbm_gbs); "
+                         f"arithmetic intensity {ai:.0f} flop/B < ridge {ridge:.0f}")
+        elif w["prec"] == "H" and w["kind"] == "gemm":
             bound = "tensor"
             peak, unit, achieved = peaks["bf16_tflops"], "TFLOP/s", flops(w) / per_launch / 1e12
             peak_note = f"dense FP16/BF16 tensor, burst ({peak_src}: MEASURED_PEAKS.json bf16_tflops)"
@@ -335,6 +356,13 @@ def run_ours(args, rank, world, local_rank):
                 extra[name] = {"error": repr(exc)}
             torch.cuda.empty_cache()
 
+    if not args.no_extra:
+        try:
+            extra["im2col"] = im2col_extra(tb, ctx, stream, torch, flush, peaks, peak_src)
+        except Exception as exc:  # noqa: BLE001
+            extra["im2col"] = {"error": repr(exc)}
+        torch.cuda.empty_cache()
+
     # North star: batched small-matrix GEMM >= 10x the naive per-matrix launch
     # loop.  Loop = one public `gemm` call per instance (first 1024 instances
     # of the 16384 x 32^3 batch, device-timed), extrapolated per instance.
@@ -366,7 +394,8 @@ def run_ours(args, rank, world, local_rank):
                    "k": w["k"], "batch": w["batch"] * (world if w["kind"] == "batched" else 1),
                    "layout": "row-major", "trans": "NN", "alpha": 1.0, "beta": 0.0,
                    "parallelism": f"column-sharded x{world}" if w["kind"] == "gemm" else f"batch-sharded x{world}",
-                   "l2": "flushed before every step (256 MiB write)"},
+                   "l2": "flushed before every step (256 MiB write + 256 MiB read of a second buffer: "
+                         "inputs evicted, no dirty lines left)"},
         "e2e": e2e,
         "gpu_launches": args.steps,
         "kernel": main["kernel"],
@@ -379,6 +408,30 @@ def run_ours(args, rank, world, local_rank):
     if extra:
         line["extra"] = extra
     return line
+
+
+def im2col_extra(tb, ctx, stream, torch, flush, peaks, peak_src) -> dict:
+    """im2col on a ResNet-style layer: 256 x 56 x 56 image,
+    3x3 kernel, pad 1, stride 1 -> 2304 x 3136 column matrix.  HBM-bound:
+    algorithmic bytes = image read + column matrix write."""
+    c, h, w_, kh, kw = 256, 56, 56, 3, 3
+    rows, cols = c * kh * kw, h * w_
+    out = {"workload": f"im2col {c}x{h}x{w_} image, {kh}x{kw} kernel, pad 1, stride 1 -> {rows}x{cols}"}
+    for prec in (tb.Precision.H, tb.Precision.S):
+        dev = ctx.torch_device
+        im = tb.buffer_from_tensor(ctx, prec, torch.rand(c * h * w_, device=dev).to(prec.torch_dtype))
+        col = tb.buffer_alloc(ctx, prec, rows * cols)
+        fn = lambda: tb.im2col(ctx, c, h, w_, kh, kw, 1, 1, 1, 1, 1, 1, im, col)  # noqa: E731
+        times = device_time(fn, 20, 3, stream, torch, flush)
+        t = sum(times) / len(times)
+        nbytes = (c * h * w_ + rows * cols) * prec.elemsize
+        gbs = nbytes / t / 1e9
+        out[prec.value] = {"us_per_call": round(t * 1e6, 2), "GB/s": round(gbs, 1),
+                           "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"],
+                                        "unit": "GB/s", "frac": round(gbs / peaks["hbm_gbs"], 4),
+                                        "peak_source": f"{peak_src}: MEASURED_PEAKS.json hbm_gbs",
+                                        "kernel": ctx.last_launch.native["kernel"]}}
+    return out
 
 
 def batched_vs_loop(tb, ctx, stream, torch, loop_instances: int = 1024) -> dict:

@@ -128,6 +128,22 @@ int tb_gemm_batched(int prec, int layout, int trans_a, int trans_b, int64_t m,
                     int offs_aligned, const tb_gemm_params* params, int flags,
                     void* stream);
 
+/*
+ * Image patches to columns — replaces extras.py:56-109 (im2col).  `im` holds
+ * channels x height x width (row-major planes) from element `im_off`; `col`
+ * receives the (channels*kernel_h*kernel_w) x (out_h*out_w) column-major
+ * matrix (ld = rows) from element `col_off`, zeros where the window falls in
+ * the padding (negative padding crops, as in the reference).  Device
+ * pointers; geometry validated by the caller (the
+ * Python routine raises the reference's UsageError / RangeError first);
+ * returns TB_ERR_INVALID for non-positive output dimensions.
+ */
+int tb_im2col(int prec, int64_t channels, int64_t height, int64_t width,
+              int64_t kernel_h, int64_t kernel_w, int64_t pad_h, int64_t pad_w,
+              int64_t stride_h, int64_t stride_w, int64_t dilation_h,
+              int64_t dilation_w, const void* im, int64_t im_off, void* col,
+              int64_t col_off, void* stream);
+
 /* Fill the record of the last launch issued from the calling thread. */
 int tb_last_launch(tb_launch_record* out);
 /* Human-readable text for a status code (static storage). */

@@ -21,6 +21,10 @@ Contents (each function cites what it restates):
   _gemm_batched_core (extras.py:188-286) on the sequential backend.
 * ``seqk_gemm`` — ctypes wrapper of oracle/gemm_seqk.c (sequential-k FMA
   chain; bit-exact checker for the GPU SGEMM contract).
+* ``port_im2col`` — the reference's ``im2col`` gather (extras.py:56-109):
+  index grids per (channel, ky, kx) row and (oy, ox) column, zero outside the
+  image, written column-major with ld = rows.  Pinned bitwise to
+  tests/golden/im2col_golden.* (made by running the reference).
 
 Parity anchor: tests/golden/ holds outputs of the reference itself
 (tests/golden/make_golden.py imports /root/reference); tests/test_oracle.py
@@ -284,3 +288,26 @@ def seqk_gemm_strided_batched(prec, row_major, trans_a, trans_b, m, n, k, alpha,
         float(beta), _ptr(c), c_offset, ldc, stride_c, batch)
     if rc:
         raise ValueError("oracle_gemm_strided_batched rejected its arguments")
+
+
+def port_im2col(image_flat: np.ndarray, im_offset: int, channels: int, height: int, width: int,
+                kernel_h: int, kernel_w: int, pad_h: int, pad_w: int, stride_h: int, stride_w: int,
+                dilation_h: int, dilation_w: int, col_flat: np.ndarray, col_offset: int) -> np.ndarray:
+    """extras.py:56-109 on host arrays: writes the (C*KH*KW) x (OH*OW)
+    column-major patch matrix into ``col_flat`` at ``col_offset`` and returns
+    ``col_flat``.  Same index arithmetic as the reference (y = ky*dh + oy*sh -
+    ph, x = kx*dw + ox*sw - pw; zero where outside the image)."""
+    span_h = dilation_h * (kernel_h - 1) + 1
+    span_w = dilation_w * (kernel_w - 1) + 1
+    out_h = (height + 2 * pad_h - span_h) // stride_h + 1
+    out_w = (width + 2 * pad_w - span_w) // stride_w + 1
+    image = image_flat[im_offset:im_offset + channels * height * width].reshape(channels, height, width)
+    y = np.arange(kernel_h)[:, None] * dilation_h + np.arange(out_h)[None, :] * stride_h - pad_h
+    x = np.arange(kernel_w)[:, None] * dilation_w + np.arange(out_w)[None, :] * stride_w - pad_w
+    y_ok, x_ok = (y >= 0) & (y < height), (x >= 0) & (x < width)
+    g = image[:, np.clip(y, 0, height - 1)[:, None, :, None], np.clip(x, 0, width - 1)[None, :, None, :]]
+    mask = (y_ok[:, None, :, None] & x_ok[None, :, None, :])[None, ...]
+    mat = np.where(mask, g, 0).astype(col_flat.dtype).reshape(channels * kernel_h * kernel_w, out_h * out_w)
+    rows, cols = mat.shape
+    col_flat[col_offset:col_offset + rows * cols] = mat.reshape(-1, order="F")
+    return col_flat

@@ -24,6 +24,7 @@
 #include "hgemm_tc_small.cuh"
 #include "hgemm_tc_2sm.cuh"
 #include "hgemm_tc_splitk.cuh"
+#include "im2col.cuh"
 #include "sgemm_tf32_tc.cuh"
 #include "sgemm_simt.cuh"
 #include "sgemm_small.cuh"
@@ -351,7 +352,7 @@ int dispatch_sgemm(const Call& c) {
     if (tiles128 >= sms) return launch_simt<128, 128, 16, 8, 8, true, 1>(c, "128");
     // < 1 wave of 128x128 (e.g. 1024^3, BASELINE C1): 64x128 4x8 (measured
     // 30.7 vs 27.8 TFLOP/s for 64x64 4x4 at 1024^3; tools/sgemm_variants.cu)
-    if (p.n >= 128 && tiles128 * 2 >= sms) return launch_simt<64, 128, 16, 4, 8, true, 2>(c, "64x128");
+    if (p.n >= 128 && tiles128 * 2 * 2 >= sms) return launch_simt<64, 128, 16, 4, 8, true, 2>(c, "64x128");
   }
   if (mwg >= 128 && nwg < 128 && tiles128 * 2 >= sms) return launch_simt<128, 64, 16, 8, 4, true, 2>(c, "128x64");
   if (mwg < 128 && nwg >= 128 && tiles128 * 2 >= sms) return launch_simt<64, 128, 16, 4, 8, true, 2>(c, "64x128");
@@ -718,6 +719,59 @@ int tb_gemm_batched(int prec, int layout, int trans_a, int trans_b, int64_t m, i
   call.p.batch = batch;
   call.offs_aligned = offs_aligned;
   return run(call);
+}
+
+int tb_im2col(int prec, int64_t channels, int64_t height, int64_t width, int64_t kernel_h, int64_t kernel_w,
+              int64_t pad_h, int64_t pad_w, int64_t stride_h, int64_t stride_w, int64_t dilation_h,
+              int64_t dilation_w, const void* im, int64_t im_off, void* col, int64_t col_off, void* stream) {
+  const int64_t lim = (1LL << 31) - 1;
+  if (channels < 1 || height < 1 || width < 1 || kernel_h < 1 || kernel_w < 1 || stride_h < 1 || stride_w < 1 ||
+      dilation_h < 1 || dilation_w < 1 || !im || !col) {
+    snprintf(g_last_err, sizeof(g_last_err), "im2col: invalid geometry");
+    return TB_ERR_INVALID;
+  }
+  const int64_t span_h = dilation_h * (kernel_h - 1) + 1, span_w = dilation_w * (kernel_w - 1) + 1;
+  const int64_t out_h = (height + 2 * pad_h - span_h) / stride_h + 1;
+  const int64_t out_w = (width + 2 * pad_w - span_w) / stride_w + 1;
+  if (height + 2 * pad_h < span_h || width + 2 * pad_w < span_w || out_h <= 0 || out_w <= 0) {
+    snprintf(g_last_err, sizeof(g_last_err), "im2col: output dimensions are not positive");
+    return TB_ERR_INVALID;
+  }
+  Im2colGeom g;
+  g.rows = channels * kernel_h * kernel_w;
+  g.cols = out_h * out_w;
+  const int64_t grid_y = (g.rows + IM2COL_TR - 1) / IM2COL_TR;
+  if (channels > lim || height > lim || width > lim || kernel_h * kernel_w > lim || height * width > lim ||
+      pad_h > lim || pad_w > lim || pad_h < -lim || pad_w < -lim || stride_h > lim || stride_w > lim || dilation_h > lim || dilation_w > lim ||
+      out_h > lim || out_w > lim || g.rows > lim || g.cols > lim || channels * height * width > lim ||
+      grid_y > 65535) {
+    snprintf(g_last_err, sizeof(g_last_err), "im2col: geometry exceeds the 32-bit index range of the kernel");
+    return TB_ERR_UNSUPPORTED;
+  }
+  g.channels = static_cast<int>(channels); g.height = static_cast<int>(height); g.width = static_cast<int>(width);
+  g.kh = static_cast<int>(kernel_h); g.kw = static_cast<int>(kernel_w);
+  g.pad_h = static_cast<int>(pad_h); g.pad_w = static_cast<int>(pad_w);
+  g.stride_h = static_cast<int>(stride_h); g.stride_w = static_cast<int>(stride_w);
+  g.dil_h = static_cast<int>(dilation_h); g.dil_w = static_cast<int>(dilation_w);
+  g.out_h = static_cast<int>(out_h); g.out_w = static_cast<int>(out_w);
+  dim3 grid(static_cast<unsigned>((g.cols + IM2COL_TQ - 1) / IM2COL_TQ), static_cast<unsigned>(grid_y));
+  dim3 block(32, IM2COL_TY);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const char* name;
+  if (prec == TB_PREC_S) {
+    im2col_kernel<uint32_t><<<grid, block, 0, st>>>(static_cast<const uint32_t*>(im) + im_off,
+                                                      static_cast<uint32_t*>(col) + col_off, g);
+    name = "im2col_b32";
+  } else if (prec == TB_PREC_H) {
+    im2col_kernel<uint16_t><<<grid, block, 0, st>>>(static_cast<const uint16_t*>(im) + im_off,
+                                                      static_cast<uint16_t*>(col) + col_off, g);
+    name = "im2col_b16";
+  } else {
+    snprintf(g_last_err, sizeof(g_last_err), "im2col: precision must be H or S");
+    return TB_ERR_UNSUPPORTED;
+  }
+  record(name, grid, block, 1, 0, g.rows * g.cols);
+  return check_launch("im2col launch");
 }
 
 int tb_last_launch(tb_launch_record* out) {

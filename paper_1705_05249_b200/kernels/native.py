@@ -45,6 +45,7 @@ TB_OK = 0
 #: Every symbol include/tbgemm.h declares (checked by tests/test_native_abi.py).
 EXPORTED_SYMBOLS = (
     "tb_gemm",
+    "tb_im2col",
     "tb_gemm_strided_batched",
     "tb_gemm_batched",
     "tb_last_launch",
@@ -123,6 +124,8 @@ def _declare(so) -> None:
         _i32, _i32, _i32, _i32, _i64, _i64, _i64, _vp,
         _vp, _vp, _i64, _vp, _vp, _i64, _vp,
         _vp, _vp, _i64, _i64, _i32, _P(TbGemmParams), _i32, _vp]
+    so.tb_im2col.restype = _i32
+    so.tb_im2col.argtypes = [_i32] + [_i64] * 11 + [_vp, _i64, _vp, _i64, _vp]
     so.tb_last_launch.restype = _i32
     so.tb_last_launch.argtypes = [_P(TbLaunchRecord)]
     so.tb_status_str.restype = ctypes.c_char_p

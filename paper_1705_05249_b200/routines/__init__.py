@@ -1,8 +1,10 @@
-"""The GEMM routine surface: gemm, gemm_batched, gemm_strided_batched and the
-Netlib host-array layer."""
+"""The GEMM routine surface: gemm, gemm_batched, gemm_strided_batched, the
+Netlib host-array layer, and im2col (the convolution-lowering routine the C3
+shapes come from)."""
 
 from .extras import gemm_batched, gemm_strided_batched
+from .im2col import im2col
 from .level3 import gemm
 from .netlib import default_context, netlib_call
 
-__all__ = ["gemm", "gemm_batched", "gemm_strided_batched", "default_context", "netlib_call"]
+__all__ = ["gemm", "gemm_batched", "gemm_strided_batched", "im2col", "default_context", "netlib_call"]

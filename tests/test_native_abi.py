@@ -13,7 +13,7 @@ HEADER = Path(__file__).resolve().parent.parent / "include" / "tbgemm.h"
 def declared_functions():
     text = HEADER.read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(tb_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(tb_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_and_binding_agree():
