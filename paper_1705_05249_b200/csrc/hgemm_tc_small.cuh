@@ -102,6 +102,60 @@ __device__ __forceinline__ void small_fill(uint8_t* smem, const __half* const (&
   }
 }
 
+// Single-K-block fills (k <= 64, every C4 case): each thread's chunk source
+// offsets, byte counts and smem offsets do not depend on the tile, only the
+// instance base pointers do — precompute them once per thread.
+template <int ROWS, int SLOT, bool MN, bool K32>
+struct SmallFillPlan {
+  static constexpr bool KM32 = K32 && !MN;
+  static constexpr int PER_T = KM32 ? ROWS / 32 : ROWS * 8 / 128;
+  int64_t eoff[PER_T];
+  uint32_t bytes[PER_T];
+  uint32_t off[PER_T];
+  __device__ __forceinline__ void init(int64_t ld, int extent, int k_left, int tid) {
+    const int q = KM32 ? (tid >> 2) : (tid >> 3);
+    const int c = KM32 ? (tid & 3) : (tid & 7);
+    const uint32_t off0 = static_cast<uint32_t>((q >> 3) * 1024 + (q & 7) * 128 + ((c ^ (q & 7)) << 4));
+#pragma unroll
+    for (int j = 0; j < PER_T; ++j) {
+      int valid;
+      if (!MN) {
+        constexpr int RSTEP = KM32 ? 32 : 16;
+        const int idx = q + (RSTEP * j) % SLOT;
+        valid = (idx < extent) ? min(8, k_left - c * 8) : 0;
+        eoff[j] = static_cast<int64_t>(idx) * ld + c * 8;
+        off[j] = off0 + j * (RSTEP * 128);
+      } else {
+        const int sub = j >> 2, mn = sub * 64 + c * 8, idx = mn % SLOT, r = q + 16 * (j & 3);
+        valid = (r < k_left) ? min(8, extent - idx) : 0;
+        eoff[j] = static_cast<int64_t>(r) * ld + idx;
+        off[j] = off0 + sub * 8192 + (j & 3) * 2048;
+      }
+      bytes[j] = valid > 0 ? static_cast<uint32_t>(valid) * 2u : 0u;
+    }
+  }
+  __device__ __forceinline__ void issue(uint8_t* smem, const __half* const (&inst)[4], const __half* any) const {
+#pragma unroll
+    for (int j = 0; j < PER_T; ++j) {
+      if (K32 && MN && (j & 3) >= 2) continue;  // K rows 32..63: never read
+      constexpr int RSTEP = KM32 ? 32 : 16;
+      const int slot = !MN ? (RSTEP * j) / SLOT : ((j >> 2) * 64 + 0) / SLOT + 0;
+      // MN-major: the 8 chunks of a 64-wide sub-tile may straddle two slots
+      // when SLOT = 32; the slot is then a per-lane value (c*8 / SLOT).
+      const __half* base;
+      if (!MN || SLOT >= 64) {
+        base = inst[slot];
+      } else {
+        const int c = threadIdx.x & 7;
+        base = inst[((j >> 2) * 64 + c * 8) / SLOT];
+      }
+      uint32_t nb = bytes[j];
+      if (base == nullptr) nb = 0;
+      cp_async_16(smem + off[j], nb ? base + eoff[j] : any, nb);
+    }
+  }
+};
+
 template <int MI, int NI, bool A_MN, bool B_MN, bool VEC, bool K32>
 __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
     hgemm_tc_small_kernel(Problem p, int64_t total_tiles) {
@@ -148,6 +202,14 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
     uint32_t ph = 0;
     int lag = 0;  // stages committed but not yet published (<= DEPTH - 1)
     int s_pub = 0;
+    const bool one_block = VEC && nkb == 1;
+    SmallFillPlan<128, MI, A_MN, K32> plan_a;
+    SmallFillPlan<BN, NI, B_MN, K32> plan_b;
+    if (one_block) {
+      const int k_left = static_cast<int>(p.k);
+      plan_a.init(p.lda, m, k_left, tid);
+      plan_b.init(p.ldb, n, k_left, tid);
+    }
     for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
       const int64_t zbase = t * P;
       const __half* ia[4];
@@ -163,8 +225,13 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
         mbar_wait(&empty[s], ph ^ 1);
         const int64_t k0 = static_cast<int64_t>(kb) * HG_BK;
         const int k_left = static_cast<int>(min64(HG_BK, p.k - k0));
-        small_fill<128, MI, A_MN, VEC, K32>(sA + s * C::A_BYTES, ia, A, p.lda, m, k0, k_left, tid);
-        small_fill<BN, NI, B_MN, VEC, K32>(sB + s * C::B_BYTES, ib, B, p.ldb, n, k0, k_left, tid);
+        if (one_block) {
+          plan_a.issue(sA + s * C::A_BYTES, ia, A);
+          plan_b.issue(sB + s * C::B_BYTES, ib, B);
+        } else {
+          small_fill<128, MI, A_MN, VEC, K32>(sA + s * C::A_BYTES, ia, A, p.lda, m, k0, k_left, tid);
+          small_fill<BN, NI, B_MN, VEC, K32>(sB + s * C::B_BYTES, ib, B, p.ldb, n, k0, k_left, tid);
+        }
         if (VEC) {
           cp_async_commit();
           if (lag == C::DEPTH - 1) {
