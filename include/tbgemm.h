@@ -144,6 +144,31 @@ int tb_im2col(int prec, int64_t channels, int64_t height, int64_t width,
               int64_t dilation_w, const void* im, int64_t im_off, void* col,
               int64_t col_off, void* stream);
 
+/*
+ * Structured level-3 helpers — the reference's transform kinds
+ * (kernels/transforms.py:21-147) used by symm/syrk/syr2k/trmm/trsm
+ * (routines/level3.py:152-537).  Column-major storage, element offsets.
+ *   kind TB_XF_COPY          dst = src                      (rows x cols)
+ *   kind TB_XF_SYMMETRIZE    dst = src's `upper` triangle mirrored (square)
+ *   kind TB_XF_TRIANGULARIZE dst = src's triangle, zeros elsewhere, unit diag
+ *   kind TB_XF_TRI_COPY      dst's triangle = src's triangle, rest untouched
+ */
+enum { TB_XF_COPY = 0, TB_XF_SYMMETRIZE = 1, TB_XF_TRIANGULARIZE = 2, TB_XF_TRI_COPY = 3 };
+int tb_transform(int prec, int kind, int64_t rows, int64_t cols, const void* src,
+                 int64_t src_off, int64_t lds, void* dst, int64_t dst_off,
+                 int64_t ldd, int upper, int unit, void* stream);
+/* FP32 staging (trsm keeps X in FP32, level3.py:474-483):
+ * to_f32 (direction 0): dst_f32 = alpha * op(src);  from_f32 (1): dst = RNE(op(src_f32)).
+ * op = transpose ? ^T : identity; rows x cols are the DESTINATION's. */
+int tb_convert_f32(int prec, int direction, int64_t rows, int64_t cols, float alpha,
+                   const void* src, int64_t src_off, int64_t lds, int transpose,
+                   void* dst, int64_t dst_off, int64_t ldd, void* stream);
+/* Substitution on one nb x nb (nb <= 64) diagonal block of a dense FP32
+ * triangular T for ncols right-hand sides X (level2.py:365-387). */
+int tb_trsm_block(int64_t nb, int64_t ncols, const float* t, int64_t t_off,
+                  int64_t ldt, float* x, int64_t x_off, int64_t ldx, int upper,
+                  int unit, void* stream);
+
 /* Fill the record of the last launch issued from the calling thread. */
 int tb_last_launch(tb_launch_record* out);
 /* Human-readable text for a status code (static storage). */

@@ -25,6 +25,7 @@
 #include "hgemm_tc_2sm.cuh"
 #include "hgemm_tc_splitk.cuh"
 #include "im2col.cuh"
+#include "structured.cuh"
 #include "sgemm_tf32_tc.cuh"
 #include "sgemm_simt.cuh"
 #include "sgemm_small.cuh"
@@ -772,6 +773,90 @@ int tb_im2col(int prec, int64_t channels, int64_t height, int64_t width, int64_t
   }
   record(name, grid, block, 1, 0, g.rows * g.cols);
   return check_launch("im2col launch");
+}
+
+static unsigned elementwise_blocks(int64_t total) {
+  const int sms = sm_count() > 0 ? sm_count() : 148;
+  const int64_t want = (total + 255) / 256, cap = static_cast<int64_t>(sms) * 16;
+  return static_cast<unsigned>(want < 1 ? 1 : (want < cap ? want : cap));
+}
+
+int tb_transform(int prec, int kind, int64_t rows, int64_t cols, const void* src, int64_t src_off, int64_t lds,
+                 void* dst, int64_t dst_off, int64_t ldd, int upper, int unit, void* stream) {
+  if (rows < 0 || cols < 0 || kind < TB_XF_COPY || kind > TB_XF_TRI_COPY || !src || !dst ||
+      (kind != TB_XF_COPY && rows != cols) || lds < (rows > 0 ? rows : 1) || ldd < (rows > 0 ? rows : 1)) {
+    snprintf(g_last_err, sizeof(g_last_err), "transform: invalid arguments");
+    return TB_ERR_INVALID;
+  }
+  if (rows == 0 || cols == 0) return TB_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const dim3 grid(elementwise_blocks(rows * cols)), block(256);
+  const char* name;
+  if (prec == TB_PREC_S) {
+    transform_kernel<uint32_t><<<grid, block, 0, st>>>(kind, rows, cols, static_cast<const uint32_t*>(src) + src_off,
+                                                       lds, static_cast<uint32_t*>(dst) + dst_off, ldd, upper, unit,
+                                                       0x3F800000u);
+    name = "transform_b32";
+  } else if (prec == TB_PREC_H) {
+    transform_kernel<uint16_t><<<grid, block, 0, st>>>(kind, rows, cols, static_cast<const uint16_t*>(src) + src_off,
+                                                       lds, static_cast<uint16_t*>(dst) + dst_off, ldd, upper, unit,
+                                                       static_cast<uint16_t>(0x3C00));
+    name = "transform_b16";
+  } else {
+    snprintf(g_last_err, sizeof(g_last_err), "transform: precision must be H or S");
+    return TB_ERR_UNSUPPORTED;
+  }
+  record(name, grid, block, 1, 0, rows * cols);
+  return check_launch("transform launch");
+}
+
+int tb_convert_f32(int prec, int direction, int64_t rows, int64_t cols, float alpha, const void* src, int64_t src_off,
+                   int64_t lds, int transpose, void* dst, int64_t dst_off, int64_t ldd, void* stream) {
+  if (rows < 0 || cols < 0 || !src || !dst || (direction != 0 && direction != 1) || ldd < (rows > 0 ? rows : 1) ||
+      lds < ((transpose ? cols : rows) > 0 ? (transpose ? cols : rows) : 1)) {
+    snprintf(g_last_err, sizeof(g_last_err), "convert_f32: invalid arguments");
+    return TB_ERR_INVALID;
+  }
+  if (rows == 0 || cols == 0) return TB_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const dim3 grid(elementwise_blocks(rows * cols)), block(256);
+  if (prec != TB_PREC_S && prec != TB_PREC_H) {
+    snprintf(g_last_err, sizeof(g_last_err), "convert_f32: precision must be H or S");
+    return TB_ERR_UNSUPPORTED;
+  }
+  if (direction == 0) {
+    float* d = static_cast<float*>(dst) + dst_off;
+    if (prec == TB_PREC_S)
+      to_f32_kernel<float><<<grid, block, 0, st>>>(rows, cols, alpha, static_cast<const float*>(src) + src_off, lds,
+                                                   transpose, d, ldd);
+    else
+      to_f32_kernel<__half><<<grid, block, 0, st>>>(rows, cols, alpha, static_cast<const __half*>(src) + src_off,
+                                                    lds, transpose, d, ldd);
+  } else {
+    const float* sp = static_cast<const float*>(src) + src_off;
+    if (prec == TB_PREC_S)
+      from_f32_kernel<float><<<grid, block, 0, st>>>(rows, cols, sp, lds, transpose,
+                                                     static_cast<float*>(dst) + dst_off, ldd);
+    else
+      from_f32_kernel<__half><<<grid, block, 0, st>>>(rows, cols, sp, lds, transpose,
+                                                      static_cast<__half*>(dst) + dst_off, ldd);
+  }
+  record(direction == 0 ? "to_f32" : "from_f32", grid, block, 1, 0, rows * cols);
+  return check_launch("convert_f32 launch");
+}
+
+int tb_trsm_block(int64_t nb, int64_t ncols, const float* t, int64_t t_off, int64_t ldt, float* x, int64_t x_off,
+                  int64_t ldx, int upper, int unit, void* stream) {
+  if (nb < 1 || nb > TRSM_MAX_NB || ncols < 0 || !t || !x || ldt < nb || ldx < nb) {
+    snprintf(g_last_err, sizeof(g_last_err), "trsm_block: invalid arguments (nb must be 1..%d)", TRSM_MAX_NB);
+    return TB_ERR_INVALID;
+  }
+  if (ncols == 0) return TB_OK;
+  const dim3 grid(static_cast<unsigned>((ncols + 127) / 128)), block(128);
+  trsm_block_kernel<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<int>(nb), ncols, t + t_off, ldt, x + x_off, ldx, upper, unit);
+  record("trsm_block", grid, block, 1, 0, ncols);
+  return check_launch("trsm_block launch");
 }
 
 int tb_last_launch(tb_launch_record* out) {

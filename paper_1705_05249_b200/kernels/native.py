@@ -39,6 +39,7 @@ __all__ = [
 PREC_H, PREC_S = 0, 1
 COL_MAJOR, ROW_MAJOR = 0, 1
 NO_TRANS, TRANS, CONJ_TRANS = 0, 1, 2
+XF_COPY, XF_SYMMETRIZE, XF_TRIANGULARIZE, XF_TRI_COPY = 0, 1, 2, 3
 FLAG_TF32, FLAG_NO_TMA, FLAG_SIMT_GENERAL, FLAG_NO_PACK, FLAG_NO_2SM, FLAG_NO_SPLITK = 1, 2, 4, 8, 16, 32
 TB_OK = 0
 
@@ -46,6 +47,9 @@ TB_OK = 0
 EXPORTED_SYMBOLS = (
     "tb_gemm",
     "tb_im2col",
+    "tb_transform",
+    "tb_convert_f32",
+    "tb_trsm_block",
     "tb_gemm_strided_batched",
     "tb_gemm_batched",
     "tb_last_launch",
@@ -126,6 +130,12 @@ def _declare(so) -> None:
         _vp, _vp, _i64, _i64, _i32, _P(TbGemmParams), _i32, _vp]
     so.tb_im2col.restype = _i32
     so.tb_im2col.argtypes = [_i32] + [_i64] * 11 + [_vp, _i64, _vp, _i64, _vp]
+    so.tb_transform.restype = _i32
+    so.tb_transform.argtypes = [_i32, _i32, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _vp]
+    so.tb_convert_f32.restype = _i32
+    so.tb_convert_f32.argtypes = [_i32, _i32, _i64, _i64, _f32, _vp, _i64, _i64, _i32, _vp, _i64, _i64, _vp]
+    so.tb_trsm_block.restype = _i32
+    so.tb_trsm_block.argtypes = [_i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _vp]
     so.tb_last_launch.restype = _i32
     so.tb_last_launch.argtypes = [_P(TbLaunchRecord)]
     so.tb_status_str.restype = ctypes.c_char_p

@@ -1,0 +1,364 @@
+"""Structured level-3 routines on the GPU GEMM.
+
+Restates pkg/src/tunedblas/routines/level3.py:152-537 — symm / hemm, syrk /
+herk, syr2k / her2k, trmm, trsm — with the same signatures, checks (order and
+text) and numerics model, for the precisions of this path (S and H; hemm /
+herk / her2k are complex-only in the reference and raise its UsageError for
+real precisions).
+
+As in the reference, every routine reduces to the GEMM: the structured
+operand is materialised (symmetrize / triangularize transforms, here CUDA
+kernels in csrc/structured.cuh) and multiplied with the tcgen05 / FFMA GEMM
+kernels; the rank-k updates compute alpha*P + beta*C into a copy of C with the
+GEMM epilogue (the reference's per-element ops) and copy back only the
+selected triangle (level3.py:233-246); trsm is the reference's blocked
+substitution (level3.py:462-537) with X in FP32 for every precision, the
+diagonal blocks solved by a substitution kernel and the off-diagonal panels
+updated by the GEMM.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from ..core import (Buffer, Context, Diagonal, Layout, Precision, Side, Transpose, Triangle,
+                    buffer_from_tensor, check_matrix)
+from ..errors import SingularMatrixError, UsageError
+from ..kernels import native
+from ..kernels.dispatch import prec_code, require_gpu
+from .common import check_logical, check_precision, scalar
+from .level3 import gemm
+
+__all__ = ["symm", "hemm", "syrk", "herk", "syr2k", "her2k", "trmm", "trsm"]
+
+_NO, _YES = Transpose.NO, Transpose.YES
+
+
+def _flip(tri: Triangle) -> Triangle:
+    return Triangle.LOWER if tri is Triangle.UPPER else Triangle.UPPER
+
+
+def _storage(layout: Layout, rows: int, cols: int) -> tuple[int, int]:
+    """Column-major (rows, cols) of a logical matrix's storage."""
+    return (rows, cols) if layout is Layout.COL_MAJOR else (cols, rows)
+
+
+def _temp(ctx: Context, precision: Precision, count: int) -> Buffer:
+    import torch
+
+    return buffer_from_tensor(ctx, precision, torch.empty(max(count, 1), dtype=precision.torch_dtype,
+                                                          device=ctx.torch_device))
+
+
+def _xf(ctx, precision, kind, rows, cols, src, src_off, lds, dst, dst_off, ldd, upper=True, unit=False):
+    st = native.lib().tb_transform(prec_code(precision), kind, rows, cols, src.data_ptr(), src_off, lds,
+                                   dst.data_ptr(), dst_off, ldd, int(upper), int(unit), ctx.stream_handle())
+    dst.mark_device_written()
+    native.check(st, "tb_transform")
+
+
+def _to_f32(ctx, precision, rows, cols, alpha, src, src_off, lds, transpose, dst, ldd):
+    st = native.lib().tb_convert_f32(prec_code(precision), 0, rows, cols, float(alpha), src.data_ptr(), src_off,
+                                     lds, int(transpose), dst.data_ptr(), 0, ldd, ctx.stream_handle())
+    dst.mark_device_written()
+    native.check(st, "tb_convert_f32")
+
+
+def _from_f32(ctx, precision, rows, cols, src, lds, transpose, dst, dst_off, ldd):
+    st = native.lib().tb_convert_f32(prec_code(precision), 1, rows, cols, 1.0, src.data_ptr(), 0, lds,
+                                     int(transpose), dst.data_ptr(), dst_off, ldd, ctx.stream_handle())
+    dst.mark_device_written()
+    native.check(st, "tb_convert_f32")
+
+
+def _place(ctx, precision, layout, src, src_off, lds, rows, cols, dst, ldd, row0, col0):
+    """Copy the logical rows x cols matrix ``src`` into logical block
+    (row0, col0) of ``dst`` (both in ``layout``)."""
+    sr, sc = _storage(layout, rows, cols)
+    off = row0 + col0 * ldd if layout is Layout.COL_MAJOR else col0 + row0 * ldd
+    _xf(ctx, precision, native.XF_COPY, sr, sc, src, src_off, lds, dst, off, ldd)
+
+
+# ---------------------------------------------------------------------------
+# symm / hemm (level3.py:156-224)
+# ---------------------------------------------------------------------------
+
+def _symm_hemm(ctx, layout, side, triangle, m, n, alpha, a, b, beta, c,
+               a_offset, lda, b_offset, ldb, c_offset, ldc):
+    precision = a.precision
+    check_precision(ctx, precision, a, b, c)
+    if m < 0 or n < 0:
+        raise UsageError("dimensions must be >= 0")
+    if m == 0 or n == 0:
+        return
+    na = m if side is Side.LEFT else n
+    lda = lda if lda is not None else na
+    ldb = ldb if ldb is not None else (m if layout is Layout.COL_MAJOR else n)
+    ldc = ldc if ldc is not None else (m if layout is Layout.COL_MAJOR else n)
+    # Structured storage under row-major: the bytes hold A^T -> flip the triangle.
+    check_matrix(a, a_offset, na, na, lda)
+    tri = _flip(triangle) if layout is Layout.ROW_MAJOR else triangle
+    check_logical(b, b_offset, m, n, ldb, layout)
+    check_logical(c, c_offset, m, n, ldc, layout)
+    alpha_v, beta_v = scalar(alpha, precision), scalar(beta, precision)
+    prec_code(precision)
+    require_gpu(ctx)
+    full = _temp(ctx, precision, na * na)
+    _xf(ctx, precision, native.XF_SYMMETRIZE, na, na, a, a_offset, lda, full, 0, na,
+        upper=tri is Triangle.UPPER)
+    # a dense symmetric matrix has the same bytes in either layout (ld = na)
+    if side is Side.LEFT:
+        gemm(ctx, layout, _NO, _NO, m, n, m, alpha_v, full, b, beta_v, c, lda=na,
+             b_offset=b_offset, ldb=ldb, c_offset=c_offset, ldc=ldc)
+    else:
+        gemm(ctx, layout, _NO, _NO, m, n, n, alpha_v, b, full, beta_v, c, a_offset=b_offset, lda=ldb,
+             ldb=na, c_offset=c_offset, ldc=ldc)
+
+
+def symm(ctx: Context, layout: Layout, side: Side, triangle: Triangle,
+         m: int, n: int, alpha, a: Buffer, b: Buffer, beta, c: Buffer, *,
+         a_offset: int = 0, lda: int | None = None, b_offset: int = 0,
+         ldb: int | None = None, c_offset: int = 0, ldc: int | None = None) -> None:
+    """C = alpha * A B + beta * C with A symmetric (either side)."""
+    _symm_hemm(ctx, layout, side, triangle, m, n, alpha, a, b, beta, c,
+               a_offset, lda, b_offset, ldb, c_offset, ldc)
+
+
+def hemm(ctx: Context, layout: Layout, side: Side, triangle: Triangle,
+         m: int, n: int, alpha, a: Buffer, b: Buffer, beta, c: Buffer, *,
+         a_offset: int = 0, lda: int | None = None, b_offset: int = 0,
+         ldb: int | None = None, c_offset: int = 0, ldc: int | None = None) -> None:
+    """C = alpha * A B + beta * C with A hermitian (complex only)."""
+    if not a.precision.is_complex:
+        raise UsageError("hemm is complex-only; use symm")
+    _symm_hemm(ctx, layout, side, triangle, m, n, alpha, a, b, beta, c,
+               a_offset, lda, b_offset, ldb, c_offset, ldc)
+
+
+# ---------------------------------------------------------------------------
+# syrk / syr2k (level3.py:231-352): alpha*P + beta*C into a copy of C, then
+# only the selected triangle is written back
+# ---------------------------------------------------------------------------
+
+def _rank_update(ctx, precision, layout, triangle, n, kk, alpha_v, beta_v, x, x_off, ldx, tx, y, y_off, ldy, ty,
+                 c, c_offset, ldc):
+    tmp = _temp(ctx, precision, n * n)
+    _xf(ctx, precision, native.XF_COPY, n, n, c, c_offset, ldc, tmp, 0, n)
+    gemm(ctx, layout, tx, ty, n, n, kk, alpha_v, x, y, beta_v, tmp, a_offset=x_off, lda=ldx,
+         b_offset=y_off, ldb=ldy, ldc=n)
+    tri = triangle if layout is Layout.COL_MAJOR else _flip(triangle)
+    _xf(ctx, precision, native.XF_TRI_COPY, n, n, tmp, 0, n, c, c_offset, ldc, upper=tri is Triangle.UPPER)
+
+
+def syrk(ctx: Context, layout: Layout, triangle: Triangle, trans: Transpose,
+         n: int, k: int, alpha, a: Buffer, beta, c: Buffer, *,
+         a_offset: int = 0, lda: int | None = None,
+         c_offset: int = 0, ldc: int | None = None) -> None:
+    """C_tri = alpha * op(A) op(A)^T + beta * C_tri."""
+    precision = a.precision
+    check_precision(ctx, precision, a, c)
+    if trans is Transpose.CONJUGATE and precision.is_complex:
+        raise UsageError("syrk takes No/Yes transpose; use herk for conjugation")
+    if n < 0 or k < 0:
+        raise UsageError("dimensions must be >= 0")
+    if n == 0:
+        return
+    a_rows, a_cols = (n, k) if trans is Transpose.NO else (k, n)
+    lda = lda if lda is not None else (a_rows if layout is Layout.COL_MAJOR else a_cols)
+    ldc = ldc if ldc is not None else n
+    check_logical(a, a_offset, a_rows, a_cols, lda, layout)
+    check_logical(c, c_offset, n, n, ldc, layout)
+    alpha_v, beta_v = scalar(alpha, precision), scalar(beta, precision)
+    prec_code(precision)
+    require_gpu(ctx)
+    tx = _NO if trans is Transpose.NO else _YES
+    ty = _YES if tx is _NO else _NO
+    _rank_update(ctx, precision, layout, triangle, n, k, alpha_v, beta_v, a, a_offset, lda, tx,
+                 a, a_offset, lda, ty, c, c_offset, ldc)
+
+
+def herk(ctx: Context, layout: Layout, triangle: Triangle, trans: Transpose,
+         n: int, k: int, alpha, a: Buffer, beta, c: Buffer, *,
+         a_offset: int = 0, lda: int | None = None,
+         c_offset: int = 0, ldc: int | None = None) -> None:
+    """C_tri = alpha * op(A) op(A)^H + beta * C_tri (complex only)."""
+    if not a.precision.is_complex:
+        raise UsageError("herk is complex-only; use syrk")
+    check_precision(ctx, a.precision, a, c)
+    prec_code(a.precision)  # complex precisions are not on this path
+
+
+def syr2k(ctx: Context, layout: Layout, triangle: Triangle, trans: Transpose,
+          n: int, k: int, alpha, a: Buffer, b: Buffer, beta, c: Buffer, *,
+          a_offset: int = 0, lda: int | None = None, b_offset: int = 0,
+          ldb: int | None = None, c_offset: int = 0, ldc: int | None = None) -> None:
+    """C_tri = alpha*(op(A) op(B)^T + op(B) op(A)^T) + beta*C_tri.
+
+    One GEMM over K-concatenated operands: [op(A) | op(B)] [op(B) | op(A)]^T."""
+    precision = a.precision
+    check_precision(ctx, precision, a, b, c)
+    if n < 0 or k < 0:
+        raise UsageError("dimensions must be >= 0")
+    if n == 0:
+        return
+    a_rows, a_cols = (n, k) if trans is Transpose.NO else (k, n)
+    lda = lda if lda is not None else (a_rows if layout is Layout.COL_MAJOR else a_cols)
+    ldb = ldb if ldb is not None else lda
+    ldc = ldc if ldc is not None else n
+    check_logical(a, a_offset, a_rows, a_cols, lda, layout)
+    check_logical(b, b_offset, a_rows, a_cols, ldb, layout)
+    check_logical(c, c_offset, n, n, ldc, layout)
+    alpha_v, beta_v = scalar(alpha, precision), scalar(beta, precision)
+    prec_code(precision)
+    require_gpu(ctx)
+    if trans is Transpose.NO:
+        xr, xc = n, 2 * k           # X = [A | B], Y = [B | A]   (logical n x 2k)
+        blocks = ((0, 0), (0, k))
+        tx, ty = _NO, _YES
+    else:
+        xr, xc = 2 * k, n           # X = [A ; B], Y = [B ; A]   (logical 2k x n)
+        blocks = ((0, 0), (k, 0))
+        tx, ty = _YES, _NO
+    ldxy = xr if layout is Layout.COL_MAJOR else xc
+    x = _temp(ctx, precision, xr * xc)
+    y = _temp(ctx, precision, xr * xc)
+    if k > 0:
+        for dst, first, second in ((x, (a, a_offset, lda), (b, b_offset, ldb)),
+                                   (y, (b, b_offset, ldb), (a, a_offset, lda))):
+            for (r0, c0), (src, off, ld) in zip(blocks, (first, second)):
+                _place(ctx, precision, layout, src, off, ld, a_rows, a_cols, dst, ldxy, r0, c0)
+    _rank_update(ctx, precision, layout, triangle, n, 2 * k, alpha_v, beta_v, x, 0, ldxy, tx,
+                 y, 0, ldxy, ty, c, c_offset, ldc)
+
+
+def her2k(ctx: Context, layout: Layout, triangle: Triangle, trans: Transpose,
+          n: int, k: int, alpha, a: Buffer, b: Buffer, beta, c: Buffer, *,
+          a_offset: int = 0, lda: int | None = None, b_offset: int = 0,
+          ldb: int | None = None, c_offset: int = 0, ldc: int | None = None) -> None:
+    """C_tri = alpha op(A) op(B)^H + conj(alpha) op(B) op(A)^H + beta C_tri (complex only)."""
+    if not a.precision.is_complex:
+        raise UsageError("her2k is complex-only; use syr2k")
+    check_precision(ctx, a.precision, a, b, c)
+    prec_code(a.precision)
+
+
+# ---------------------------------------------------------------------------
+# trmm / trsm (level3.py:389-537)
+# ---------------------------------------------------------------------------
+
+def _triangular(ctx, precision, layout, triangle, trans, diagonal, na, a, a_offset, lda):
+    """Materialised triangular M (column-major na x na, ld na) and whether
+    op(A) is M^T: the bytes hold A (column-major) or A^T (row-major)."""
+    lda = lda if lda is not None else na
+    check_matrix(a, a_offset, na, na, lda)
+    tri = _flip(triangle) if layout is Layout.ROW_MAJOR else triangle
+    m_full = _temp(ctx, precision, na * na)
+    _xf(ctx, precision, native.XF_TRIANGULARIZE, na, na, a, a_offset, lda, m_full, 0, na,
+        upper=tri is Triangle.UPPER, unit=diagonal is Diagonal.UNIT)
+    if layout is Layout.COL_MAJOR:
+        eff_t = trans is not Transpose.NO          # M = A
+    else:
+        eff_t = trans is Transpose.NO              # M = A^T
+    upper_op = (tri is Triangle.UPPER) != eff_t   # is op(A) upper triangular?
+    return m_full, eff_t, upper_op
+
+
+def _gemm_flag(layout: Layout, eff_t: bool) -> Transpose:
+    """Transpose flag that makes the column-major M read as op(A) in ``layout``."""
+    if layout is Layout.COL_MAJOR:
+        return _YES if eff_t else _NO
+    return _NO if eff_t else _YES
+
+
+def trmm(ctx: Context, layout: Layout, side: Side, triangle: Triangle,
+         trans: Transpose, diagonal: Diagonal, m: int, n: int, alpha,
+         a: Buffer, b: Buffer, *, a_offset: int = 0, lda: int | None = None,
+         b_offset: int = 0, ldb: int | None = None) -> None:
+    """B = alpha * op(A) B (side LEFT) or alpha * B op(A) (side RIGHT), in place."""
+    precision = a.precision
+    check_precision(ctx, precision, a, b)
+    if m < 0 or n < 0:
+        raise UsageError("dimensions must be >= 0")
+    if m == 0 or n == 0:
+        return
+    na = m if side is Side.LEFT else n
+    ldb = ldb if ldb is not None else (m if layout is Layout.COL_MAJOR else n)
+    check_logical(b, b_offset, m, n, ldb, layout)
+    check_matrix(a, a_offset, na, na, lda if lda is not None else na)  # level3.py:400-401
+    prec_code(precision)
+    require_gpu(ctx)
+    m_full, eff_t, _ = _triangular(ctx, precision, layout, triangle, trans, diagonal, na, a, a_offset, lda)
+    alpha_v = scalar(alpha, precision)
+    # B is both input and output: the GEMM reads a copy
+    sr, sc = _storage(layout, m, n)
+    b_in = _temp(ctx, precision, m * n)
+    _xf(ctx, precision, native.XF_COPY, sr, sc, b, b_offset, ldb, b_in, 0, sr)
+    flag = _gemm_flag(layout, eff_t)
+    zero = precision.compute_dtype.type(0)
+    if side is Side.LEFT:
+        gemm(ctx, layout, flag, _NO, m, n, m, alpha_v, m_full, b_in, zero, b, lda=na, ldb=sr,
+             c_offset=b_offset, ldc=ldb)
+    else:
+        gemm(ctx, layout, _NO, flag, m, n, n, alpha_v, b_in, m_full, zero, b, lda=sr, ldb=na,
+             c_offset=b_offset, ldc=ldb)
+
+
+def trsm(ctx: Context, layout: Layout, side: Side, triangle: Triangle,
+         trans: Transpose, diagonal: Diagonal, m: int, n: int, alpha,
+         a: Buffer, b: Buffer, *, a_offset: int = 0, lda: int | None = None,
+         b_offset: int = 0, ldb: int | None = None, block_size: int = 32) -> None:
+    """Solve op(A) X = alpha B (LEFT) or X op(A) = alpha B (RIGHT), X into B.
+
+    Blocked substitution: diagonal blocks solve by substitution, off-diagonal
+    panels update through the GEMM (X kept in FP32 for every precision, as in
+    the reference, and rounded once on the way back into B)."""
+    precision = a.precision
+    check_precision(ctx, precision, a, b)
+    if m < 0 or n < 0:
+        raise UsageError("dimensions must be >= 0")
+    if m == 0 or n == 0:
+        return
+    na = m if side is Side.LEFT else n
+    ldb = ldb if ldb is not None else (m if layout is Layout.COL_MAJOR else n)
+    check_logical(b, b_offset, m, n, ldb, layout)
+    check_matrix(a, a_offset, na, na, lda if lda is not None else na)  # level3.py:400-401
+    prec_code(precision)
+    require_gpu(ctx)
+    m_full, eff_t, upper_op = _triangular(ctx, precision, layout, triangle, trans, diagonal, na, a,
+                                          a_offset, lda)
+    alpha_v = scalar(alpha, precision)
+    S = Precision.S
+    # T = op(A) (LEFT) or op(A)^T (RIGHT: X op(A) = aB <=> op(A)^T X^T = aB^T), FP32 column-major
+    right = side is Side.RIGHT
+    t32 = _temp(ctx, S, na * na)
+    _to_f32(ctx, precision, na, na, 1.0, m_full, 0, na, eff_t != right, t32, na)
+    upper = upper_op != right
+    if diagonal is Diagonal.NON_UNIT:
+        diag = _temp(ctx, S, na)
+        _xf(ctx, S, native.XF_COPY, 1, na, t32, 0, na + 1, diag, 0, 1)
+        zeros = np.nonzero(diag.device_tensor()[:na].cpu().numpy() == 0)[0]
+        if zeros.size:
+            raise SingularMatrixError(int(zeros[0]))
+    # X = alpha * B (LEFT, m x n) or alpha * B^T (RIGHT, n x m), FP32 column-major
+    xr, xc = (m, n) if not right else (n, m)
+    x = _temp(ctx, S, xr * xc)
+    transpose_b = (layout is Layout.ROW_MAJOR) != right
+    _to_f32(ctx, precision, xr, xc, alpha_v, b, b_offset, ldb, transpose_b, x, xr)
+    nb = max(1, min(int(block_size), 64))
+    blocks = list(range(0, na, nb))
+    so = native.lib()
+    C = Layout.COL_MAJOR
+    for i0 in (reversed(blocks) if upper else blocks):
+        i1 = min(i0 + nb, na)
+        st = so.tb_trsm_block(i1 - i0, xc, t32.data_ptr(), i0 + i0 * na, na, x.data_ptr(), i0, xr,
+                              int(upper), int(diagonal is Diagonal.UNIT), ctx.stream_handle())
+        native.check(st, "tb_trsm_block")
+        if upper and i0 > 0:        # X[:i0] -= T[:i0, i0:i1] X[i0:i1]
+            gemm(ctx, C, _NO, _NO, i0, xc, i1 - i0, -1.0, t32, x, 1.0, x,
+                 a_offset=i0 * na, lda=na, b_offset=i0, ldb=xr, c_offset=0, ldc=xr)
+        elif not upper and i1 < na:  # X[i1:] -= T[i1:, i0:i1] X[i0:i1]
+            gemm(ctx, C, _NO, _NO, na - i1, xc, i1 - i0, -1.0, t32, x, 1.0, x,
+                 a_offset=i1 + i0 * na, lda=na, b_offset=i0, ldb=xr, c_offset=i1, ldc=xr)
+    # back into B with one rounding
+    br, bc = _storage(layout, m, n)
+    _from_f32(ctx, precision, br, bc, x, xr, transpose_b, b, b_offset, ldb)
