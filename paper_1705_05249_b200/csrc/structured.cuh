@@ -137,4 +137,47 @@ __global__ void trsm_block_kernel(int nb, int64_t ncols, const float* __restrict
   for (int i = 0; i < nb; ++i) xc[i] = xv[i];
 }
 
+// Register-resident version for full NB x NB blocks (NB = 16 / 32): both
+// loops fully unrolled, x stays in registers; same operation order as
+// trsm_block_kernel.
+template <int NB>
+__global__ void __launch_bounds__(64) trsm_block_reg_kernel(int64_t ncols, const float* __restrict__ t, int64_t ldt,
+                                                            float* __restrict__ x, int64_t ldx, int upper, int unit) {
+  __shared__ float ts[NB * NB];
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int j = e / NB, i = e - j * NB;
+    ts[i + j * NB] = t[i + j * ldt];
+  }
+  __syncthreads();
+  const int64_t col = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (col >= ncols) return;
+  float xv[NB];
+  float* xc = x + col * ldx;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) xv[i] = xc[i];
+  if (!upper) {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      float s = 0.0f;
+#pragma unroll
+      for (int k = 0; k < i; ++k) s = __fmaf_rn(ts[i + k * NB], xv[k], s);
+      float v = __fsub_rn(xv[i], s);
+      if (!unit) v = __fdiv_rn(v, ts[i + i * NB]);
+      xv[i] = v;
+    }
+  } else {
+#pragma unroll
+    for (int i = NB - 1; i >= 0; --i) {
+      float s = 0.0f;
+#pragma unroll
+      for (int k = i + 1; k < NB; ++k) s = __fmaf_rn(ts[i + k * NB], xv[k], s);
+      float v = __fsub_rn(xv[i], s);
+      if (!unit) v = __fdiv_rn(v, ts[i + i * NB]);
+      xv[i] = v;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NB; ++i) xc[i] = xv[i];
+}
+
 }  // namespace tb

@@ -852,9 +852,18 @@ int tb_trsm_block(int64_t nb, int64_t ncols, const float* t, int64_t t_off, int6
     return TB_ERR_INVALID;
   }
   if (ncols == 0) return TB_OK;
-  const dim3 grid(static_cast<unsigned>((ncols + 127) / 128)), block(128);
-  trsm_block_kernel<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<int>(nb), ncols, t + t_off, ldt, x + x_off, ldx, upper, unit);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (nb == 32 || nb == 16) {  // register-resident full blocks, 64-thread CTAs
+    const dim3 grid(static_cast<unsigned>((ncols + 63) / 64)), block(64);
+    if (nb == 32)
+      trsm_block_reg_kernel<32><<<grid, block, 0, st>>>(ncols, t + t_off, ldt, x + x_off, ldx, upper, unit);
+    else
+      trsm_block_reg_kernel<16><<<grid, block, 0, st>>>(ncols, t + t_off, ldt, x + x_off, ldx, upper, unit);
+    record(nb == 32 ? "trsm_block_reg32" : "trsm_block_reg16", grid, block, 1, 0, ncols);
+    return check_launch("trsm_block launch");
+  }
+  const dim3 grid(static_cast<unsigned>((ncols + 63) / 64)), block(64);
+  trsm_block_kernel<<<grid, block, 0, st>>>(static_cast<int>(nb), ncols, t + t_off, ldt, x + x_off, ldx, upper, unit);
   record("trsm_block", grid, block, 1, 0, ncols);
   return check_launch("trsm_block launch");
 }

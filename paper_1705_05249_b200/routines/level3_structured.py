@@ -25,8 +25,8 @@ from ..core import (Buffer, Context, Diagonal, Layout, Precision, Side, Transpos
                     buffer_from_tensor, check_matrix)
 from ..errors import SingularMatrixError, UsageError
 from ..kernels import native
-from ..kernels.dispatch import prec_code, require_gpu
-from .common import check_logical, check_precision, scalar
+from ..kernels.dispatch import gemm_native, prec_code, require_gpu
+from .common import check_logical, check_precision, get_store, scalar
 from .level3 import gemm
 
 __all__ = ["symm", "hemm", "syrk", "herk", "syr2k", "her2k", "trmm", "trsm"]
@@ -345,20 +345,41 @@ def trsm(ctx: Context, layout: Layout, side: Side, triangle: Triangle,
     transpose_b = (layout is Layout.ROW_MAJOR) != right
     _to_f32(ctx, precision, xr, xc, alpha_v, b, b_offset, ldb, transpose_b, x, xr)
     nb = max(1, min(int(block_size), 64))
-    blocks = list(range(0, na, nb))
+    # Two-level blocking (same math as the reference's single level; only the
+    # update order differs): chunks of NB2 rows are solved block by block with
+    # updates confined to the chunk, then one K = NB2 GEMM updates every
+    # remaining row — X is re-read na/NB2 times instead of na/nb times.
+    nb2 = max(nb, (256 // nb) * nb)
     so = native.lib()
     C = Layout.COL_MAJOR
-    for i0 in (reversed(blocks) if upper else blocks):
-        i1 = min(i0 + nb, na)
-        st = so.tb_trsm_block(i1 - i0, xc, t32.data_ptr(), i0 + i0 * na, na, x.data_ptr(), i0, xr,
-                              int(upper), int(diagonal is Diagonal.UNIT), ctx.stream_handle())
-        native.check(st, "tb_trsm_block")
-        if upper and i0 > 0:        # X[:i0] -= T[:i0, i0:i1] X[i0:i1]
-            gemm(ctx, C, _NO, _NO, i0, xc, i1 - i0, -1.0, t32, x, 1.0, x,
-                 a_offset=i0 * na, lda=na, b_offset=i0, ldb=xr, c_offset=0, ldc=xr)
-        elif not upper and i1 < na:  # X[i1:] -= T[i1:, i0:i1] X[i0:i1]
-            gemm(ctx, C, _NO, _NO, na - i1, xc, i1 - i0, -1.0, t32, x, 1.0, x,
-                 a_offset=i1 + i0 * na, lda=na, b_offset=i0, ldb=xr, c_offset=i1, ldc=xr)
+    # Panel updates go straight to the C-ABI (their operands are this
+    # routine's own validated temps); FP32 built-in configuration.
+    cfg = get_store(ctx).resolve("gemm", S, ctx.device, (na, xc, nb))[0]
+    unit = int(diagonal is Diagonal.UNIT)
+
+    def update(r0, r1, k0, k1):
+        """X[r0:r1] -= T[r0:r1, k0:k1] X[k0:k1]"""
+        if r1 > r0 and k1 > k0:
+            gemm_native(ctx, S, C, _NO, _NO, r1 - r0, xc, k1 - k0, -1.0, t32, r0 + k0 * na, na, x, k0, xr,
+                        1.0, x, r0, xr, cfg)
+
+    chunks = list(range(0, na, nb2))
+    for c0 in (reversed(chunks) if upper else chunks):
+        c1 = min(c0 + nb2, na)
+        blocks = list(range(c0, c1, nb))
+        for i0 in (reversed(blocks) if upper else blocks):
+            i1 = min(i0 + nb, c1)
+            st = so.tb_trsm_block(i1 - i0, xc, t32.data_ptr(), i0 + i0 * na, na, x.data_ptr(), i0, xr,
+                                  int(upper), unit, ctx.stream_handle())
+            native.check(st, "tb_trsm_block")
+            if upper:
+                update(c0, i0, i0, i1)
+            else:
+                update(i1, c1, i0, i1)
+        if upper:
+            update(0, c0, c0, c1)
+        else:
+            update(c1, na, c0, c1)
     # back into B with one rounding
     br, bc = _storage(layout, m, n)
     _from_f32(ctx, precision, br, bc, x, xr, transpose_b, b, b_offset, ldb)
