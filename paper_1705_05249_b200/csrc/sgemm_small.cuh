@@ -23,17 +23,22 @@ namespace tb {
 template <int MI, int NI, int TM = 4, int TN = 4>
 struct SsCfg {
   static constexpr int KC = 32;
+  static constexpr int KCP = KC + 4;                    // padded K-contiguous row (floats)
   static constexpr int TY = MI / TM, TX = NI / TN;      // threads per instance = TX*TY
   static constexpr int QM = TM / 4, QN = TN / 4;        // 4x4 sub-blocks, spaced MI/QM, NI/QN
   static constexpr int TPI = TX * TY;
   static constexpr int G = 256 / TPI;                   // instances per stage
-  // smem per instance slot: A as [KC][MI] (M-contig) or [MI][KC] with the
-  // 16-byte chunks XOR-swizzled by (row/4)%8 (K-contig, conflict-free reads)
-  static constexpr int A_ELEMS = KC * MI;
-  static constexpr int B_ELEMS = KC * NI;
+  // smem per instance slot: A as [KC][MI] (M-contig) or [MI][KCP]
+  // (K-contig, rows padded by 4 floats: 16-byte aligned chunks, and the
+  // fragment reads are quarter-warp broadcasts, so the padding costs no
+  // conflicts while every read address is base + immediate)
+  static constexpr int A_ELEMS_M = KC * MI, A_ELEMS_K = MI * KCP;
+  static constexpr int B_ELEMS_N = KC * NI, B_ELEMS_K = NI * KCP;
+  static constexpr int A_ELEMS = A_ELEMS_K > A_ELEMS_M ? A_ELEMS_K : A_ELEMS_M;
+  static constexpr int B_ELEMS = B_ELEMS_K > B_ELEMS_N ? B_ELEMS_K : B_ELEMS_N;
   static constexpr int STAGE_FLOATS = G * (A_ELEMS + B_ELEMS);
   // 3-4 stages, <= ~100 KB so two CTAs share an SM
-  static constexpr int STAGES = (4 * STAGE_FLOATS * 4 <= 100 * 1024) ? 4 : 3;
+  static constexpr int STAGES = (4 * STAGE_FLOATS * 4 <= 110 * 1024) ? 4 : 3;
   static constexpr int SMEM_BYTES = STAGES * STAGE_FLOATS * 4;
   // 8x8 micro-tiles need > 128 registers: one CTA per SM
   static constexpr int MINB = (TM * TN >= 64) ? 1 : 2;
@@ -45,10 +50,8 @@ __global__ void __launch_bounds__(256, (SsCfg<MI, NI, TM, TN>::MINB))
   using C = SsCfg<MI, NI, TM, TN>;
   constexpr int QM = C::QM, QN = C::QN;
   constexpr int KC = C::KC, G = C::G, STAGES = C::STAGES;
-  // K-contiguous slot layout: element (row, kk) of a [rows][KC] tile
-  auto kidx = [](int row, int kk) {
-    return row * KC + ((((kk >> 2) ^ ((row >> 2) & 7)) << 2) | (kk & 3));
-  };
+  // K-contiguous slot layout: element (row, kk) of a [rows][KCP] tile
+  auto kidx = [](int row, int kk) { return row * C::KCP + kk; };
   extern __shared__ __align__(16) float smem_f[];
 
   const int tid = threadIdx.x;
@@ -73,6 +76,39 @@ __global__ void __launch_bounds__(256, (SsCfg<MI, NI, TM, TN>::MINB))
   // constant, so only the instance pointers are computed per stage.
   constexpr int A_CH = MI * KC / 4, B_CH = NI * KC / 4;
   static_assert(A_CH % 256 == 0 && B_CH % 256 == 0, "whole chunks per thread");
+  // Single-chunk K (k <= KC, every C4 case): each thread's chunk offsets and
+  // valid counts are stage-invariant — computed once into a compact plan
+  // (32-bit offsets + 3-bit counts), so a stage only adds instance bases.
+  constexpr int NA = G * A_CH / 256, NB = G * B_CH / 256;
+  static_assert(NA + NB <= 10, "plan packs 3-bit counts into one word");
+  const bool planned = kchunks == 1 && p.lda * (AK ? MI : KC) < (1LL << 31) &&
+                       p.ldb * (!BNC ? NI : KC) < (1LL << 31);
+  int32_t plan_off[NA + NB];
+  uint32_t plan_valid = 0;
+  if (planned) {
+    const int k_left = static_cast<int>(p.k);
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+      const int r = (256 * j) % A_CH + tid;
+      int row, kk, valid;
+      if (AK) { row = r / (KC / 4); kk = (r % (KC / 4)) * 4; }
+      else { kk = r / (MI / 4); row = (r % (MI / 4)) * 4; }
+      if (AK) { valid = (row < m) ? max(0, min(4, k_left - kk)) : 0; plan_off[j] = static_cast<int32_t>(row * p.lda + kk); }
+      else { valid = (kk < k_left) ? max(0, min(4, m - row)) : 0; plan_off[j] = static_cast<int32_t>(kk * p.lda + row); }
+      plan_valid |= static_cast<uint32_t>(valid) << (3 * j);
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int r = (256 * j) % B_CH + tid;
+      int col, kk, valid;
+      if (!BNC) { col = r / (KC / 4); kk = (r % (KC / 4)) * 4; }
+      else { kk = r / (NI / 4); col = (r % (NI / 4)) * 4; }
+      if (!BNC) { valid = (col < n) ? max(0, min(4, k_left - kk)) : 0; plan_off[NA + j] = static_cast<int32_t>(col * p.ldb + kk); }
+      else { valid = (kk < k_left) ? max(0, min(4, n - col)) : 0; plan_off[NA + j] = static_cast<int32_t>(kk * p.ldb + col); }
+      plan_valid |= static_cast<uint32_t>(valid) << (3 * (NA + j));
+    }
+  }
+
   auto issue = [&](int64_t gi, int kc, int s) {
     const int64_t k0 = static_cast<int64_t>(kc) * KC;
     const int k_left = static_cast<int>(min64(KC, p.k - k0));
@@ -84,6 +120,31 @@ __global__ void __launch_bounds__(256, (SsCfg<MI, NI, TM, TN>::MINB))
       const int64_t z = gi * G + g;
       ia[g] = z < p.batch ? A + inst_off(p.a_off, p.stride_a, p.a_offs, z) : nullptr;
       ib[g] = z < p.batch ? B + inst_off(p.b_off, p.stride_b, p.b_offs, z) : nullptr;
+    }
+    if (planned) {
+#pragma unroll
+      for (int j = 0; j < NA; ++j) {
+        const int g = (256 * j) / A_CH;
+        const int r = (256 * j) % A_CH + tid;
+        const int row = AK ? r / (KC / 4) : (r % (MI / 4)) * 4;
+        const int kk = AK ? (r % (KC / 4)) * 4 : r / (MI / 4);
+        uint32_t valid = (plan_valid >> (3 * j)) & 7u;
+        if (ia[g] == nullptr) valid = 0;
+        float* dst = st + g * C::A_ELEMS + (AK ? kidx(row, kk) : kk * MI + row);
+        cp_async_16(dst, valid ? ia[g] + plan_off[j] : A, valid * 4u);
+      }
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int g = (256 * j) / B_CH;
+        const int r = (256 * j) % B_CH + tid;
+        const int col = !BNC ? r / (KC / 4) : (r % (NI / 4)) * 4;
+        const int kk = !BNC ? (r % (KC / 4)) * 4 : r / (NI / 4);
+        uint32_t valid = (plan_valid >> (3 * (NA + j))) & 7u;
+        if (ib[g] == nullptr) valid = 0;
+        float* dst = st + G * C::A_ELEMS + g * C::B_ELEMS + (!BNC ? kidx(col, kk) : kk * NI + col);
+        cp_async_16(dst, valid ? ib[g] + plan_off[NA + j] : B, valid * 4u);
+      }
+      return;
     }
 #pragma unroll
     for (int j = 0; j < G * A_CH / 256; ++j) {
