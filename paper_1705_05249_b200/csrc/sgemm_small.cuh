@@ -80,11 +80,11 @@ __global__ void __launch_bounds__(256, (SsCfg<MI, NI, TM, TN>::MINB))
   // valid counts are stage-invariant — computed once into a compact plan
   // (32-bit offsets + 3-bit counts), so a stage only adds instance bases.
   constexpr int NA = G * A_CH / 256, NB = G * B_CH / 256;
-  static_assert(NA + NB <= 10, "plan packs 3-bit counts into one word");
+  static_assert(NA + NB <= 21, "plan packs 3-bit counts into one 64-bit word");
   const bool planned = kchunks == 1 && p.lda * (AK ? MI : KC) < (1LL << 31) &&
                        p.ldb * (!BNC ? NI : KC) < (1LL << 31);
   int32_t plan_off[NA + NB];
-  uint32_t plan_valid = 0;
+  uint64_t plan_valid = 0;
   if (planned) {
     const int k_left = static_cast<int>(p.k);
 #pragma unroll
@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(256, (SsCfg<MI, NI, TM, TN>::MINB))
       else { kk = r / (MI / 4); row = (r % (MI / 4)) * 4; }
       if (AK) { valid = (row < m) ? max(0, min(4, k_left - kk)) : 0; plan_off[j] = static_cast<int32_t>(row * p.lda + kk); }
       else { valid = (kk < k_left) ? max(0, min(4, m - row)) : 0; plan_off[j] = static_cast<int32_t>(kk * p.lda + row); }
-      plan_valid |= static_cast<uint32_t>(valid) << (3 * j);
+      plan_valid |= static_cast<uint64_t>(valid) << (3 * j);
     }
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256, (SsCfg<MI, NI, TM, TN>::MINB))
       else { kk = r / (NI / 4); col = (r % (NI / 4)) * 4; }
       if (!BNC) { valid = (col < n) ? max(0, min(4, k_left - kk)) : 0; plan_off[NA + j] = static_cast<int32_t>(col * p.ldb + kk); }
       else { valid = (kk < k_left) ? max(0, min(4, n - col)) : 0; plan_off[NA + j] = static_cast<int32_t>(kk * p.ldb + col); }
-      plan_valid |= static_cast<uint32_t>(valid) << (3 * (NA + j));
+      plan_valid |= static_cast<uint64_t>(valid) << (3 * (NA + j));
     }
   }
 
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(256, (SsCfg<MI, NI, TM, TN>::MINB))
         const int r = (256 * j) % A_CH + tid;
         const int row = AK ? r / (KC / 4) : (r % (MI / 4)) * 4;
         const int kk = AK ? (r % (KC / 4)) * 4 : r / (MI / 4);
-        uint32_t valid = (plan_valid >> (3 * j)) & 7u;
+        uint32_t valid = static_cast<uint32_t>(plan_valid >> (3 * j)) & 7u;
         if (ia[g] == nullptr) valid = 0;
         float* dst = st + g * C::A_ELEMS + (AK ? kidx(row, kk) : kk * MI + row);
         cp_async_16(dst, valid ? ia[g] + plan_off[j] : A, valid * 4u);
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256, (SsCfg<MI, NI, TM, TN>::MINB))
         const int r = (256 * j) % B_CH + tid;
         const int col = !BNC ? r / (KC / 4) : (r % (NI / 4)) * 4;
         const int kk = !BNC ? (r % (KC / 4)) * 4 : r / (NI / 4);
-        uint32_t valid = (plan_valid >> (3 * (NA + j))) & 7u;
+        uint32_t valid = static_cast<uint32_t>(plan_valid >> (3 * (NA + j))) & 7u;
         if (ib[g] == nullptr) valid = 0;
         float* dst = st + G * C::A_ELEMS + g * C::B_ELEMS + (!BNC ? kidx(col, kk) : kk * NI + col);
         cp_async_16(dst, valid ? ib[g] + plan_off[NA + j] : B, valid * 4u);

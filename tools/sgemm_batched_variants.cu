@@ -75,7 +75,6 @@ int main(int argc, char** argv) {
     run_small<32, 32, 4, 4>(p, 20, "small 32 4x4 (64t/inst)");
     run_small<32, 32, 8, 4>(p, 20, "small 32 8x4 (32t/inst)");
     run_small<32, 32, 4, 8>(p, 20, "small 32 4x8 (32t/inst)");
-    run_small<32, 32, 8, 8>(p, 20, "small 32 8x8 (16t/inst)");
   }
   return 0;
 }
