@@ -221,6 +221,23 @@ __device__ __forceinline__ bool elect_one() {
 
 namespace tb {
 // ---------------------------------------------------------------------------
+// FP32 register-tile outer product on the paired FFMA pipe (FFMA2).
+// acc2[i2][j] holds rows (2*i2, 2*i2+1) of column j.  Each lane of
+// fma.rn.f32x2 is an ordinary round-to-nearest FP32 fma, so the chain per
+// element is bitwise the scalar __fmaf_rn chain; FFMA2 just issues two of
+// them per instruction (b[j] is the broadcast scalar operand in SASS).
+// ---------------------------------------------------------------------------
+template <int TM, int TN>
+__device__ __forceinline__ void outer_ffma2(float2 (&acc2)[TM / 2][TN], const float (&af)[TM],
+                                            const float (&bf)[TN]) {
+#pragma unroll
+  for (int i2 = 0; i2 < TM / 2; ++i2)
+#pragma unroll
+    for (int j = 0; j < TN; ++j)
+      acc2[i2][j] = __ffma2_rn(make_float2(bf[j], bf[j]), make_float2(af[2 * i2], af[2 * i2 + 1]),
+                               acc2[i2][j]);
+}
+// ---------------------------------------------------------------------------
 // cp.async (LDGSTS): 16-byte global -> shared, zero-filling past src_bytes
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gsrc, uint32_t src_bytes) {

@@ -14,7 +14,8 @@
 // Structure: BM x BN CTA tile, BK-deep stages double-buffered in shared
 // memory, register prefetch of the next stage while the current one is
 // consumed, TM x TN register micro-tile built from 4x4 sub-blocks read with
-// 128-bit LDS, 128-bit LDG when the operands are 16-byte aligned.
+// 128-bit LDS, 128-bit LDG when the operands are 16-byte aligned; the
+// outer product issues on FFMA2 (two bitwise-FFMA lanes per instruction).
 #pragma once
 
 #include "common.cuh"
@@ -141,11 +142,11 @@ __global__ void __launch_bounds__(SimtShape<BM, BN, BK, TM, TN>::NT, MINB)
   const int ty = threadIdx.x % S::TY;  // M index (fastest -> coalesced C columns)
   const int tx = threadIdx.x / S::TY;  // N index
 
-  float acc[TM][TN];
+  float2 acc2[TM / 2][TN];   // rows (2*i2, 2*i2+1) of column j, see outer_ffma2
 #pragma unroll
-  for (int i = 0; i < TM; ++i)
+  for (int i = 0; i < TM / 2; ++i)
 #pragma unroll
-    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
+    for (int j = 0; j < TN; ++j) acc2[i][j] = make_float2(0.0f, 0.0f);
 
   if (!epi.skip_ab) {
     const float* A = static_cast<const float*>(p.a) + inst_off(p.a_off, p.stride_a, p.a_offs, z);
@@ -191,10 +192,7 @@ __global__ void __launch_bounds__(SimtShape<BM, BN, BK, TM, TN>::NT, MINB)
             const float4 t = *reinterpret_cast<const float4*>(bs + kk * S::LDB_S + q * (BN / S::QN) + tx * 4);
             bf[q * 4 + 0] = t.x; bf[q * 4 + 1] = t.y; bf[q * 4 + 2] = t.z; bf[q * 4 + 3] = t.w;
           }
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < TN; ++j) acc[i][j] = __fmaf_rn(af[i], bf[j], acc[i][j]);
+          outer_ffma2<TM, TN>(acc2, af, bf);
         }
       } else {
         // K tail: exactly kcur more FMAs (no zero padding — keeps the chain
@@ -212,10 +210,7 @@ __global__ void __launch_bounds__(SimtShape<BM, BN, BK, TM, TN>::NT, MINB)
             const float4 t = *reinterpret_cast<const float4*>(bs + kk * S::LDB_S + q * (BN / S::QN) + tx * 4);
             bf[q * 4 + 0] = t.x; bf[q * 4 + 1] = t.y; bf[q * 4 + 2] = t.z; bf[q * 4 + 3] = t.w;
           }
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < TN; ++j) acc[i][j] = __fmaf_rn(af[i], bf[j], acc[i][j]);
+          outer_ffma2<TM, TN>(acc2, af, bf);
         }
       }
       if (kt + 1 < ktiles) {
@@ -228,6 +223,7 @@ __global__ void __launch_bounds__(SimtShape<BM, BN, BK, TM, TN>::NT, MINB)
   }
 
   // Epilogue: rows (q*BM/QM + ty*4 + r), cols (q*BN/QN + tx*4 + c).
+#define ACC2(i, j) (((i) & 1) ? acc2[(i) >> 1][j].y : acc2[(i) >> 1][j].x)
   float* C = static_cast<float*>(p.c) + inst_off(p.c_off, p.stride_c, p.c_offs, z);
   const int64_t cbase_off = inst_off(p.c_off, p.stride_c, p.c_offs, z);
   const bool cvec = ((cbase_off & 3) == 0) && ((p.ldc & 3) == 0);
@@ -245,23 +241,24 @@ __global__ void __launch_bounds__(SimtShape<BM, BN, BK, TM, TN>::NT, MINB)
           float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
           if (epi.reads_c()) cv = *reinterpret_cast<const float4*>(ccol + row);
           float4 o;
-          o.x = epi.apply(acc[qm * 4 + 0][qn * 4 + c], cv.x);
-          o.y = epi.apply(acc[qm * 4 + 1][qn * 4 + c], cv.y);
-          o.z = epi.apply(acc[qm * 4 + 2][qn * 4 + c], cv.z);
-          o.w = epi.apply(acc[qm * 4 + 3][qn * 4 + c], cv.w);
+          o.x = epi.apply(ACC2(qm * 4 + 0, qn * 4 + c), cv.x);
+          o.y = epi.apply(ACC2(qm * 4 + 1, qn * 4 + c), cv.y);
+          o.z = epi.apply(ACC2(qm * 4 + 2, qn * 4 + c), cv.z);
+          o.w = epi.apply(ACC2(qm * 4 + 3, qn * 4 + c), cv.w);
           *reinterpret_cast<float4*>(ccol + row) = o;
         } else {
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
             if (row + r < rows_m) {
               const float cv = epi.reads_c() ? ccol[row + r] : 0.0f;
-              ccol[row + r] = epi.apply(acc[qm * 4 + r][qn * 4 + c], cv);
+              ccol[row + r] = epi.apply(ACC2(qm * 4 + r, qn * 4 + c), cv);
             }
           }
         }
       }
     }
   }
+#undef ACC2
 }
 
 }  // namespace tb

@@ -29,6 +29,7 @@
 #include "sgemm_tf32_tc.cuh"
 #include "sgemm_simt.cuh"
 #include "sgemm_small.cuh"
+#include "sgemm_tma.cuh"
 #include "tbgemm.h"
 
 using namespace tb;
@@ -117,10 +118,11 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-// 3-D tensor map (FP16 or FP32): dims {contig, other, batch}, box {box0, box1, 1}, SW128.
+// 3-D tensor map (FP16 or FP32): dims {contig, other, batch}, box {box0, box1, 1}, SW128 by default.
 int make_map(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t batch, uint64_t ld,
              uint64_t stride, uint32_t box0, uint32_t box1,
-             CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT16, uint64_t es = 2) {
+             CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT16, uint64_t es = 2,
+             CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) {
     snprintf(g_last_err, sizeof(g_last_err), "cuTensorMapEncodeTiled entry point unavailable");
@@ -133,7 +135,7 @@ int make_map(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint6
   cuuint32_t box[3] = {box0, box1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     snprintf(g_last_err, sizeof(g_last_err), "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
@@ -204,6 +206,65 @@ int launch_simt(const Call& c, const char* tag) {
   (void)tag;
   record(name, grid, block, 1, 0, blocks);
   return check_launch("sgemm_simt launch");
+}
+
+// TMA-fed FFMA2 SGEMM (sgemm_tma.cuh).  M/N-contiguous operands: box
+// {ROWS, 32} without swizzle; K-contiguous: box {32, ROWS} SWIZZLE_128B.
+template <int BM, int BN, int TM, int TN, int ST, bool AMN, bool BMN>
+int launch_stma(const Call& c) {
+  using Cfg = TmaSgemmCfg<BM, BN, 32, TM, TN, ST, AMN, BMN>;
+  const Problem& p = c.p;
+  const float* A = static_cast<const float*>(p.a) + p.a_off;
+  const float* B = static_cast<const float*>(p.b) + p.b_off;
+  const CUtensorMapDataType F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  CUtensorMap ta, tbm;
+  memset(&ta, 0, sizeof(ta));
+  memset(&tbm, 0, sizeof(tbm));
+  int rc = AMN ? make_map(&ta, A, p.m, p.k, p.batch, p.lda, p.stride_a, BM, 32, F32, 4, CU_TENSOR_MAP_SWIZZLE_NONE)
+               : make_map(&ta, A, p.k, p.m, p.batch, p.lda, p.stride_a, 32, BM, F32, 4, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc != TB_OK) return rc;
+  rc = BMN ? make_map(&tbm, B, p.n, p.k, p.batch, p.ldb, p.stride_b, BN, 32, F32, 4, CU_TENSOR_MAP_SWIZZLE_NONE)
+           : make_map(&tbm, B, p.k, p.n, p.batch, p.ldb, p.stride_b, 32, BN, F32, 4, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc != TB_OK) return rc;
+  const int tiles_m = static_cast<int>((p.m + BM - 1) / BM);
+  const int tiles_n = static_cast<int>((p.n + BN - 1) / BN);
+  const int64_t blocks = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
+  if (blocks > 0x7fffffffLL) return TB_ERR_INVALID;
+  auto kern = sgemm_tma_kernel<BM, BN, 32, TM, TN, ST, AMN, BMN, 2>;
+  static SmemAttr attr;  // per instantiation, per device
+  if (int rc2 = ensure_smem(attr, kern, Cfg::SMEM_BYTES)) return rc2;
+  dim3 grid(static_cast<unsigned>(blocks)), block(Cfg::NT);
+  kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, 8);
+  char name[64];
+  snprintf(name, sizeof(name), "sgemm_tma_%dx%dx32_%dx%d_%c%c", BM, BN, TM, TN, AMN ? 'm' : 'k', BMN ? 'n' : 'k');
+  record(name, grid, block, 1, Cfg::SMEM_BYTES, blocks);
+  return check_launch("sgemm_tma launch");
+}
+
+// Route to the TMA kernel: returns -1 when the problem does not qualify.
+int dispatch_sgemm_tma(const Call& c) {
+  const Problem& p = c.p;
+  const bool amn = !p.a_kcontig, bmn = p.b_ncontig;
+  if (!amn && !bmn) return -1;  // both K-contiguous: FFMA2 pairs would need register shuffles
+  if (p.a_offs || p.b_offs || p.alphas || p.betas || p.k <= 0 || p.alpha == 0.0f) return -1;
+  if ((p.lda % 4) || (p.ldb % 4) || !aligned_elems(p.a, p.a_off, 4, 16) || !aligned_elems(p.b, p.b_off, 4, 16))
+    return -1;
+  if (p.batch > 1 && ((p.stride_a % 4) || (p.stride_b % 4))) return -1;
+  if (p.m > 0x7fffff00LL || p.n > 0x7fffff00LL || p.k > 0x7fffff00LL || p.batch > 0x7fffffffLL) return -1;
+  const int sms = sm_count() > 0 ? sm_count() : 148;
+  const int64_t tiles128 = ((p.m + 127) / 128) * ((p.n + 127) / 128) * p.batch;
+  // Measured on B200 (tools/sgemm_ms_bench.cu): with >= 4 waves of 128x128
+  // tiles the big tiles win (64x128 8x8 when both operands are M/N-contiguous:
+  // 66 TFLOP/s at 8192^3); below that 64x64 tiles of 4x8 (8x4) micro-tiles
+  // keep every SM busy (1024^3 37.6, C3 (4096,128,9216) 34.8 TFLOP/s).
+  if (tiles128 >= 4 * sms) {
+    if (amn && bmn) return launch_stma<64, 128, 8, 8, 4, true, true>(c);
+    if (amn) return launch_stma<128, 128, 16, 8, 2, true, false>(c);
+    return launch_stma<128, 128, 8, 16, 2, false, true>(c);
+  }
+  if (amn && bmn) return launch_stma<64, 64, 4, 8, 3, true, true>(c);
+  if (amn) return launch_stma<64, 64, 4, 8, 3, true, false>(c);
+  return launch_stma<64, 64, 8, 4, 4, false, true>(c);
 }
 
 template <int MI, int NI, int TM, int TN, bool AK, bool BNC>
@@ -336,6 +397,11 @@ int dispatch_sgemm(const Call& c) {
     if (c.params->VWM == 1 && c.params->VWN == 1) vec = false;
   }
   if (!vec) return launch_simt<64, 64, 16, 4, 4, false, 2>(c, "general");
+  const bool small_inst = p.k > 0 && p.m <= 64 && p.n <= 64 && (p.batch > 1 || p.k <= 4096);
+  if (!small_inst && !(c.flags & TB_FLAG_SIMT_GENERAL)) {
+    const int rc = dispatch_sgemm_tma(c);
+    if (rc >= 0) return rc;
+  }
   // Small instances: persistent cp.async-pipelined kernel (bitwise identical).
   if (p.k > 0 && p.m <= 64 && p.n <= 64 && (p.batch > 1 || p.k <= 4096)) {
     if (p.m <= 32 && p.n <= 32) return launch_ss_layout<32, 32, 4, 4>(c);
