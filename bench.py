@@ -377,6 +377,11 @@ def run_ours(args, rank, world, local_rank):
     traffic = load_traffic(main["kernel"])
     if traffic is not None:
         main["roofline"]["traffic"] = traffic
+    for ex in extra.values():
+        if isinstance(ex, dict) and isinstance(ex.get("roofline"), dict):
+            t = load_traffic(ex["roofline"].get("kernel", ""))
+            if t is not None:
+                ex["roofline"]["traffic"] = t
     line = {
         "metric": METRIC,
         "value": round(main["gflops"], 2),

@@ -28,7 +28,7 @@
 //     one 128-bit read yields 4 consecutive kk of one row.
 // FFMA2 pairs: along M (A fragments come as float4 along M) unless A is
 // K-contiguous, then along N (B must be N-contiguous; both-K-contiguous
-// operands use sgemm_ms.cuh).
+// operands use the register-staged kernel, sgemm_simt.cuh).
 #pragma once
 
 #include "common.cuh"
@@ -45,7 +45,7 @@ struct TmaSgemmCfg {
   static constexpr int A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-  static_assert(A_MN || B_MN, "both K-contiguous: use the cp.async kernel");
+  static_assert(A_MN || B_MN, "both K-contiguous: use sgemm_simt.cuh");
   static_assert(BK == 32, "K-contiguous tiles are 128-byte SWIZZLE_128B rows");
   static_assert(TM % 4 == 0 && TN % 4 == 0 && NT % 32 == 0, "tile shape");
   static_assert(A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0, "1024-byte aligned stage tiles");

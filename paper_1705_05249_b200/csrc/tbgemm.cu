@@ -257,7 +257,8 @@ int dispatch_sgemm_tma(const Call& c) {
   // tiles the big tiles win (64x128 8x8 when both operands are M/N-contiguous:
   // 66 TFLOP/s at 8192^3); below that 64x64 tiles of 4x8 (8x4) micro-tiles
   // keep every SM busy (1024^3 37.6, C3 (4096,128,9216) 34.8 TFLOP/s).
-  if (tiles128 >= 4 * sms) {
+  const bool one_tile = p.m <= 64 && p.n <= 64;  // batched small instances: one 64x64 tile each
+  if (tiles128 >= 4 * sms && !one_tile) {
     if (amn && bmn) return launch_stma<64, 128, 8, 8, 4, true, true>(c);
     if (amn) return launch_stma<128, 128, 16, 8, 2, true, false>(c);
     return launch_stma<128, 128, 8, 16, 2, false, true>(c);
@@ -405,8 +406,14 @@ int dispatch_sgemm(const Call& c) {
   // Small instances: persistent cp.async-pipelined kernel (bitwise identical).
   if (p.k > 0 && p.m <= 64 && p.n <= 64 && (p.batch > 1 || p.k <= 4096)) {
     if (p.m <= 32 && p.n <= 32) return launch_ss_layout<32, 32, 4, 4>(c);
-    // 33..64: the tiled kernel with a 4x8 micro-tile measured faster than the
-    // cp.async small kernel for 64^3 instances (tools/sgemm_batched_variants.cu)
+    // 33..64: one 64x64 tile per instance on the TMA-fed FFMA2 kernel (3-D
+    // tensor maps over the batch) when the operands allow tensor maps; else
+    // the register-staged tiled kernel with a 4x8 micro-tile (measured faster
+    // than the cp.async small kernel for 64^3, tools/sgemm_batched_variants.cu)
+    if (!(c.flags & TB_FLAG_SIMT_GENERAL)) {
+      const int rc = dispatch_sgemm_tma(c);
+      if (rc >= 0) return rc;
+    }
     return launch_simt<64, 64, 16, 4, 8, true, 2>(c, "64x64 4x8");
   }
   const int sms = sm_count() > 0 ? sm_count() : 148;

@@ -20,7 +20,7 @@
 // outer product issues as FFMA2 (outer_ffma2, common.cuh).
 #pragma once
 
-#include "common.cuh"
+#include "../paper_1705_05249_b200/csrc/common.cuh"
 
 namespace tb {
 

@@ -3,7 +3,7 @@
 #include <cstdio>
 #include <cstring>
 #include <vector>
-#include "../paper_1705_05249_b200/csrc/sgemm_ms.cuh"
+#include "sgemm_ms.cuh"
 #include "../paper_1705_05249_b200/csrc/sgemm_simt.cuh"
 #include "../paper_1705_05249_b200/csrc/sgemm_tma.cuh"
 #include <cudaTypedefs.h>
