@@ -211,11 +211,40 @@ __global__ void __launch_bounds__(256, (SsCfg<MI, NI, TM, TN>::MINB))
   int64_t gi = blockIdx.x;        // current compute stage
   int kc = 0;
 
-  float acc[TM][TN];
+  // Accumulators as FFMA2 pairs: along M when A fragments arrive as float4
+  // along M (!AK), along N when only B's do (AK && BNC); scalar FFMA when both
+  // operands are K-contiguous (pairs would need register moves).  Either way
+  // each element is the same ascending-k chain of RN fmas.
+  constexpr int PAIR = !AK ? 1 : (BNC ? 2 : 0);  // 1: (r, r+1), 2: (c, c+1), 0: scalar
+  float2 acc2[TM * TN / 2];
+  auto acc_ref = [&](int r, int c) -> float& {
+    if (PAIR == 2) return (c & 1) ? acc2[r * (TN / 2) + (c >> 1)].y : acc2[r * (TN / 2) + (c >> 1)].x;
+    return (r & 1) ? acc2[(r >> 1) * TN + c].y : acc2[(r >> 1) * TN + c].x;
+  };
+  auto fma_step = [&](const float (&a)[TM], const float (&b)[TN]) {
+    if constexpr (PAIR == 1) {
 #pragma unroll
-  for (int r = 0; r < TM; ++r)
+      for (int r2 = 0; r2 < TM / 2; ++r2)
 #pragma unroll
-    for (int c = 0; c < TN; ++c) acc[r][c] = 0.0f;
+        for (int c = 0; c < TN; ++c)
+          acc2[r2 * TN + c] = __ffma2_rn(make_float2(b[c], b[c]), make_float2(a[2 * r2], a[2 * r2 + 1]),
+                                         acc2[r2 * TN + c]);
+    } else if constexpr (PAIR == 2) {
+#pragma unroll
+      for (int r = 0; r < TM; ++r)
+#pragma unroll
+        for (int c2 = 0; c2 < TN / 2; ++c2)
+          acc2[r * (TN / 2) + c2] = __ffma2_rn(make_float2(a[r], a[r]), make_float2(b[2 * c2], b[2 * c2 + 1]),
+                                               acc2[r * (TN / 2) + c2]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < TM; ++r)
+#pragma unroll
+        for (int c = 0; c < TN; ++c) acc_ref(r, c) = __fmaf_rn(a[r], b[c], acc_ref(r, c));
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < TM * TN / 2; ++i) acc2[i] = make_float2(0.0f, 0.0f);
 
   for (int64_t si = 0; si < total; ++si) {
     cp_async_wait<STAGES - 2>();
@@ -271,12 +300,8 @@ __global__ void __launch_bounds__(256, (SsCfg<MI, NI, TM, TN>::MINB))
           }
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int r = 0; r < TM; ++r)
-#pragma unroll
-          for (int c = 0; c < TN; ++c) acc[r][c] = __fmaf_rn(a[q][r], b[q][c], acc[r][c]);
-        };
+      for (int q = 0; q < 4; ++q) fma_step(a[q], b[q]);
+    };
     int kk = 0;
     if (k_left == KC) {
 #pragma unroll
@@ -291,10 +316,7 @@ __global__ void __launch_bounds__(256, (SsCfg<MI, NI, TM, TN>::MINB))
       for (int r = 0; r < TM; ++r) a[r] = AK ? as[kidx(rowof(r), kk)] : as[kk * MI + rowof(r)];
 #pragma unroll
       for (int c = 0; c < TN; ++c) b[c] = !BNC ? bs[kidx(colof(c), kk)] : bs[kk * NI + colof(c)];
-#pragma unroll
-      for (int r = 0; r < TM; ++r)
-#pragma unroll
-        for (int c = 0; c < TN; ++c) acc[r][c] = __fmaf_rn(a[r], b[c], acc[r][c]);
+      fma_step(a, b);
     }
 
     if (kc == kchunks - 1) {
@@ -320,17 +342,17 @@ __global__ void __launch_bounds__(256, (SsCfg<MI, NI, TM, TN>::MINB))
               float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
               if (epi.reads_c()) cv = *reinterpret_cast<const float4*>(cc);
               float4 o;
-              o.x = epi.apply(acc[h * 4 + 0][c], cv.x);
-              o.y = epi.apply(acc[h * 4 + 1][c], cv.y);
-              o.z = epi.apply(acc[h * 4 + 2][c], cv.z);
-              o.w = epi.apply(acc[h * 4 + 3][c], cv.w);
+              o.x = epi.apply(acc_ref(h * 4 + 0, c), cv.x);
+              o.y = epi.apply(acc_ref(h * 4 + 1, c), cv.y);
+              o.z = epi.apply(acc_ref(h * 4 + 2, c), cv.z);
+              o.w = epi.apply(acc_ref(h * 4 + 3, c), cv.w);
               *reinterpret_cast<float4*>(cc) = o;
             } else {
 #pragma unroll
               for (int r = 0; r < 4; ++r) {
                 if (r0 + r < m) {
                   const float cvs = epi.reads_c() ? cc[r] : 0.0f;
-                  cc[r] = epi.apply(acc[h * 4 + r][c], cvs);
+                  cc[r] = epi.apply(acc_ref(h * 4 + r, c), cvs);
                 }
               }
             }
@@ -338,9 +360,7 @@ __global__ void __launch_bounds__(256, (SsCfg<MI, NI, TM, TN>::MINB))
         }
       }
 #pragma unroll
-      for (int r = 0; r < TM; ++r)
-#pragma unroll
-        for (int c = 0; c < TN; ++c) acc[r][c] = 0.0f;
+      for (int i = 0; i < TM * TN / 2; ++i) acc2[i] = make_float2(0.0f, 0.0f);
     }
     advance(gi, kc);
   }
