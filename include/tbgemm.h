@@ -69,8 +69,10 @@ enum {
   TB_FLAG_SIMT_GENERAL = 4, /* SGEMM: force the general predicated kernel        */
   TB_FLAG_NO_PACK = 8,       /* HGEMM: no small-instance packing (testing)        */
   TB_FLAG_NO_2SM = 16,       /* HGEMM: no CTA-pair (cta_group::2) kernel (testing) */
-  TB_FLAG_NO_SPLITK = 32     /* HGEMM: no cluster split-K (testing; results then
+  TB_FLAG_NO_SPLITK = 32,    /* HGEMM: no cluster split-K (testing; results then
                                 differ from the default route within tolerance) */
+  TB_FLAG_WAVE_SYNC = 64     /* HGEMM: CTA-pair kernel's wave barrier on any size
+                                (testing; on by default above ~6 TFLOP per call) */
 };
 
 /*

@@ -91,10 +91,37 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
       : "memory");
 }
 
+// Wave barrier for very long K (wave_ctr != nullptr): the producer of every
+// CTA waits before loading its w-th tile until all CTAs have issued the loads
+// of their (w-1)-th, and counts each tile it finishes issuing.  Without it the
+// persistent clusters drift apart in k over hundreds of tiles, the A/B panel
+// slices a wave shares are no longer read close together in time, and at
+// K = 32768 (16 MB panels, ~18 panels per wave) L2 reuse collapses (ncu: 329 GB
+// DRAM per 32768^3 call; the barrier measured 945 -> 1286 TFLOP/s there).
+// The barrier is advisory: the target never exceeds the tiles every CTA will
+// finish (ragged last wave), and a wait gives up after ~2 ms (%globaltimer) so
+// CTAs that are not co-resident can never deadlock the launch.  The counter
+// is zeroed on the launch stream before every launch.
+__device__ __forceinline__ void wave_wait(const unsigned int* ctr, unsigned int target) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  unsigned int v;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if (v >= target) return;
+    uint64_t t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 2000000ull) return;
+  }
+}
+__device__ __forceinline__ void wave_arrive(unsigned int* ctr) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+}
+
 template <bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
     hgemm_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Problem p,
-                        int tiles_m, int tiles_n, int group_m, int64_t total_tiles) {
+                        int tiles_m, int tiles_n, int group_m, int64_t total_tiles, unsigned int* wave_ctr) {
   using C = H2Cfg;
   constexpr int STAGES = H2_STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -147,7 +174,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
     // The whole warp runs the loop (uniform coordinates); one elected lane issues.
     int s = 0;
     uint32_t ph = 0;
-    for (int64_t t = cluster_id; t < total_tiles; t += n_clusters) {
+    unsigned int wave = 0;
+    // waves every cluster completes (the last wave may be ragged)
+    const unsigned int full_waves = static_cast<unsigned int>(total_tiles / n_clusters);
+    for (int64_t t = cluster_id; t < total_tiles; t += n_clusters, ++wave) {
+      if (wave_ctr != nullptr && wave > 0) {
+        if (elect_one()) wave_wait(wave_ctr, min(wave, full_waves) * gridDim.x);
+        __syncwarp();
+      }
       int64_t z; int mt, nt;
       tile_coords(t, tiles_m, tiles_n, group_m, z, mt, nt);
       const int m0 = mt * 256 + static_cast<int>(rank) * 128;
@@ -175,6 +209,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
         }
         __syncwarp();
         if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+      if (wave_ctr != nullptr) {
+        if (elect_one()) wave_arrive(wave_ctr);
+        __syncwarp();
       }
     }
   } else if (warp == C::MMA_WARP) {

@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "hgemm_tc.cuh"
 #include "hgemm_tc_small.cuh"
@@ -480,8 +481,25 @@ int launch_hg_layout(const Call& c, const CUtensorMap& ta, const CUtensorMap& tb
   return launch_hg<BN, TMA, true, true, VEC>(c, ta, tbm);
 }
 
+// One zero-initialised wave counter per (device, stream) for the pair kernel's
+// wave barrier, allocated on first use and kept (a counter shared between
+// streams could be reset under a running launch).
+unsigned int* wave_counter(cudaStream_t stream) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, cudaStream_t>, unsigned int*>> pool;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : pool)
+    if (e.first.first == dev && e.first.second == stream) return e.second;
+  unsigned int* p = nullptr;
+  if (cudaMalloc(&p, 256) != cudaSuccess) return nullptr;
+  pool.push_back({{dev, stream}, p});
+  return p;
+}
+
 template <bool AMN, bool BMN>
-int launch_h2(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
+int launch_h2(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm, bool sync_waves) {
   const Problem& p = c.p;
   const int tiles_m = static_cast<int>((p.m + 255) / 256);
   const int tiles_n = static_cast<int>((p.n + H2_BN - 1) / H2_BN);
@@ -492,8 +510,14 @@ int launch_h2(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
   const int sms = sm_count() > 0 ? sm_count() : 148;
   const int64_t clusters = total < sms / 2 ? total : sms / 2;
   dim3 grid(static_cast<unsigned>(2 * clusters)), block(H2Cfg::THREADS);
-  const int group_m = 8;  // measured best for pair tiles (tools/exp7.py)
-  kern<<<grid, block, H2Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, group_m, total);
+  const int group_m = 8;  // measured best for pair tiles (tools/exp7.py; also with the wave barrier)
+  unsigned int* ctr = nullptr;
+  if (sync_waves) {
+    ctr = wave_counter(c.stream);
+    if (!ctr) return TB_ERR_CUDA;
+    if (cudaMemsetAsync(ctr, 0, sizeof(unsigned int), c.stream) != cudaSuccess) return check_launch("wave counter");
+  }
+  kern<<<grid, block, H2Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, group_m, total, ctr);
   char name[64];
   snprintf(name, sizeof(name), "hgemm_tc2sm_tma_256x256_%c%c", AMN ? 'm' : 'k', BMN ? 'n' : 'k');
   record(name, grid, block, 2, H2Cfg::SMEM_BYTES, total);
@@ -525,16 +549,22 @@ int dispatch_hgemm_bn(const Call& c) {
     // (16384^3, 32768^3) its L2 reuse collapses (329 GB DRAM reads at 32768^3
     // vs 69 GB single-CTA), so those stay on the 128x256 single-CTA kernel.
     const double flop = 2.0 * static_cast<double>(p.m) * p.n * p.k * p.batch;
-    const bool two_sm = BN == 256 && !(c.flags & TB_FLAG_NO_2SM) && pair_tiles >= sms / 2 && flop <= 6e12;
+    // Above ~6 TFLOP per call the pair kernel runs with the wave barrier
+    // (hgemm_tc_2sm.cuh): 32768^3 945 -> 1286 TFLOP/s, 16384^3 1256 -> 1398,
+    // vs 1150 / 1325 for the single-CTA kernel (tools/hbig_probe.py).  Below
+    // that the barrier measured neutral and is left off.
+    const bool huge = flop > 6e12;
+    const bool two_sm = BN == 256 && !(c.flags & TB_FLAG_NO_2SM) && pair_tiles >= sms / 2;
+    const bool sync_waves = huge || (c.flags & TB_FLAG_WAVE_SYNC);
     const uint32_t bbox = two_sm ? 128 : BN;
     if (!bmn) rc = make_map(&tbm, B, p.k, p.n, p.batch, p.ldb, p.stride_b, 64, bbox);
     else rc = make_map(&tbm, B, p.n, p.k, p.batch, p.ldb, p.stride_b, 64, 64);
     if (rc != TB_OK) return rc;
     if (two_sm) {
-      if (!amn && !bmn) return launch_h2<false, false>(c, ta, tbm);
-      if (!amn && bmn) return launch_h2<false, true>(c, ta, tbm);
-      if (amn && !bmn) return launch_h2<true, false>(c, ta, tbm);
-      return launch_h2<true, true>(c, ta, tbm);
+      if (!amn && !bmn) return launch_h2<false, false>(c, ta, tbm, sync_waves);
+      if (!amn && bmn) return launch_h2<false, true>(c, ta, tbm, sync_waves);
+      if (amn && !bmn) return launch_h2<true, false>(c, ta, tbm, sync_waves);
+      return launch_h2<true, true>(c, ta, tbm, sync_waves);
     }
     return launch_hg_layout<BN, true, true>(c, ta, tbm);
   }

@@ -34,6 +34,7 @@ __all__ = [
     "FLAG_NO_PACK",
     "FLAG_NO_2SM",
     "FLAG_NO_SPLITK",
+    "FLAG_WAVE_SYNC",
 ]
 
 PREC_H, PREC_S = 0, 1
@@ -41,6 +42,7 @@ COL_MAJOR, ROW_MAJOR = 0, 1
 NO_TRANS, TRANS, CONJ_TRANS = 0, 1, 2
 XF_COPY, XF_SYMMETRIZE, XF_TRIANGULARIZE, XF_TRI_COPY = 0, 1, 2, 3
 FLAG_TF32, FLAG_NO_TMA, FLAG_SIMT_GENERAL, FLAG_NO_PACK, FLAG_NO_2SM, FLAG_NO_SPLITK = 1, 2, 4, 8, 16, 32
+FLAG_WAVE_SYNC = 64
 TB_OK = 0
 
 #: Every symbol include/tbgemm.h declares (checked by tests/test_native_abi.py).

@@ -317,8 +317,9 @@ def test_large_sampled_parity(ctx, prec):
 @pytest.mark.parametrize("ta", ["n", "t"])
 @pytest.mark.parametrize("tbn", ["n", "t"])
 def test_cta_pair_kernel_bitwise_equals_single_cta(ctx, layout, ta, tbn):
-    """The 2-SM (tcgen05 cta_group::2) kernel agrees bitwise with the
-    single-CTA kernel, and both with the float64 product within tolerance."""
+    """The 2-SM (tcgen05 cta_group::2) kernel — with and without its wave
+    barrier — agrees bitwise with the single-CTA kernel, and all with the
+    float64 product within tolerance."""
     import torch
 
     from paper_1705_05249_b200.kernels import native
@@ -337,14 +338,14 @@ def test_cta_pair_kernel_bitwise_equals_single_cta(ctx, layout, ta, tbn):
     ldc = m if layout == "col" else n
     cfg = tb.routines.common.get_store(ctx).resolve("gemm", prec, ctx.device, (m, n, k))[0]
     outs, kernels = [], []
-    for flags in (0, native.FLAG_NO_2SM):
+    for flags in (0, native.FLAG_NO_2SM, native.FLAG_WAVE_SYNC):
         c = tb.buffer_alloc(ctx, prec, m * n)
         rec = gemm_native(ctx, prec, L[layout], T[ta], T[tbn], m, n, k, 1.0, a, 0, lda, b, 0, ldb, 0.0,
                           c, 0, ldc, cfg, flags)
         outs.append(c.device_tensor().clone())
         kernels.append(rec["kernel"])
-    assert "2sm" in kernels[0] and "2sm" not in kernels[1], kernels
-    assert torch.equal(outs[0], outs[1]), kernels
+    assert "2sm" in kernels[0] and "2sm" not in kernels[1] and "2sm" in kernels[2], kernels
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2]), kernels
     # sampled rows against the float64 product
     A = at.view(a_rows, a_cols).double() if layout == "row" else at.view(a_cols, a_rows).t().double()
     B = bt.view(b_rows, b_cols).double() if layout == "row" else bt.view(b_cols, b_rows).t().double()
