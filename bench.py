@@ -3,7 +3,7 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--workload hgemm|sgemm|batched_h32|batched_s32|batched_h64|batched_s64|
-                                sgemm_c1|hgemm_c3|sgemm_c3]
+                                sgemm_c1|hgemm_c3|sgemm_c3|hgemm_c5|sgemm_c5]
                     [--no-extra] [--no-cpu-baseline]
 
 A "step" is one call of the hot path on one batch of synthetic input:
@@ -66,6 +66,10 @@ WORKLOADS = {
     "sgemm_c1": dict(kind="gemm", prec="S", m=1024, n=1024, k=1024, batch=1),
     "hgemm_c3": dict(kind="gemm", prec="H", m=4096, n=128, k=9216, batch=1),
     "sgemm_c3": dict(kind="gemm", prec="S", m=4096, n=128, k=9216, batch=1),
+    # C5: the large GEMM (per rank under torchrun: weak scaling, each rank its
+    # own 32768-column block)
+    "hgemm_c5": dict(kind="gemm", prec="H", m=32768, n=32768, k=32768, batch=1),
+    "sgemm_c5": dict(kind="gemm", prec="S", m=32768, n=32768, k=32768, batch=1),
 }
 
 
@@ -347,7 +351,8 @@ def run_ours(args, rank, world, local_rank):
             if name == args.workload:
                 continue
             try:
-                r = measure(name, max(5, min(args.steps, 20)), args.warmup)
+                big = WORKLOADS[name]["m"] >= 32768
+                r = measure(name, 3 if big else max(5, min(args.steps, 20)), min(args.warmup, 3) if big else args.warmup)
                 extra[name] = {"workload": describe(r["w"]), "value": round(r["gflops"], 1),
                                "unit": "GFLOPS", "ms_per_step": round(r["total"] / max(1, len(r["times"])) * 1e3, 4),
                                "roofline": r["roofline"], "clocks": r["clocks"]}
@@ -374,12 +379,12 @@ def run_ours(args, rank, world, local_rank):
 
     if rank != 0:
         return None
-    traffic = load_traffic(main["kernel"])
+    traffic = load_traffic(args.workload, main["kernel"])
     if traffic is not None:
         main["roofline"]["traffic"] = traffic
-    for ex in extra.values():
+    for name, ex in extra.items():
         if isinstance(ex, dict) and isinstance(ex.get("roofline"), dict):
-            t = load_traffic(ex["roofline"].get("kernel", ""))
+            t = load_traffic(name, ex["roofline"].get("kernel", ""))
             if t is not None:
                 ex["roofline"]["traffic"] = t
     line = {
@@ -464,17 +469,22 @@ def batched_vs_loop(tb, ctx, stream, torch, loop_instances: int = 1024) -> dict:
     return out
 
 
-def load_traffic(kernel: str):
-    """dram bytes per launch from the committed ncu capture, if one matches."""
+def load_traffic(workload: str, kernel: str):
+    """dram bytes per launch from the committed ncu capture of this workload
+    (profiles/traffic.json: {workload: {"kernel": name, "bytes": B}}), used
+    only when the capture was of the same kernel."""
     path = ROOT / "profiles" / "traffic.json"
     if not path.exists():
         return None
     try:
         with open(path) as fh:
             doc = json.load(fh)
-        return doc.get(kernel)
-    except Exception:  # noqa: BLE001
+    except (OSError, ValueError):
         return None
+    ent = doc.get(workload)
+    if isinstance(ent, dict) and ent.get("kernel") == kernel:
+        return ent.get("bytes")
+    return None
 
 
 # ---------------------------------------------------------------------------
