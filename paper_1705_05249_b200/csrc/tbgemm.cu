@@ -243,7 +243,8 @@ int launch_stma(const Call& c) {
 }
 
 // Route to the TMA kernel: returns -1 when the problem does not qualify.
-int dispatch_sgemm_tma(const Call& c) {
+// tile: 0 = by shape (no tuned configuration), 1 = large tiles, 2 = 64x64.
+int dispatch_sgemm_tma(const Call& c, int tile) {
   const Problem& p = c.p;
   const bool amn = !p.a_kcontig, bmn = p.b_ncontig;
   if (!amn && !bmn) return -1;  // both K-contiguous: FFMA2 pairs would need register shuffles
@@ -259,7 +260,8 @@ int dispatch_sgemm_tma(const Call& c) {
   // 66 TFLOP/s at 8192^3); below that 64x64 tiles of 4x8 (8x4) micro-tiles
   // keep every SM busy (1024^3 37.6, C3 (4096,128,9216) 34.8 TFLOP/s).
   const bool one_tile = p.m <= 64 && p.n <= 64;  // batched small instances: one 64x64 tile each
-  if (tiles128 >= 4 * sms && !one_tile) {
+  const bool big = tile == 0 ? tiles128 >= 4 * sms : tile == 1;
+  if (big && !one_tile) {
     if (amn && bmn) return launch_stma<64, 128, 8, 8, 4, true, true>(c);
     if (amn) return launch_stma<128, 128, 16, 8, 2, true, false>(c);
     return launch_stma<128, 128, 8, 16, 2, false, true>(c);
@@ -392,16 +394,24 @@ int dispatch_sgemm(const Call& c) {
   // Parameter mapping: VWM = VWN = 1 asks for scalar loads; MWG /
   // NWG choose the CTA tile.  Every instantiation yields bitwise-identical
   // results (sequential-k chain), so the mapping is free to follow speed.
+  // A tuned configuration (override / tuning DB; NULL when the built-in
+  // default applies) picks the kernel family by KWG — 32: the TMA-fed kernel
+  // (32-deep stages), 16: the register-staged kernel — and the tile by MWG x
+  // NWG; without one, the shape decides (measured crossovers below).
   int mwg = 128, nwg = 128;
+  bool want_tma = true;
+  int tma_tile = 0;
   if (c.params) {
     mwg = c.params->MWG;
     nwg = c.params->NWG;
     if (c.params->VWM == 1 && c.params->VWN == 1) vec = false;
+    want_tma = c.params->KWG >= 32;
+    tma_tile = (mwg >= 128 && nwg >= 128) ? 1 : 2;
   }
   if (!vec) return launch_simt<64, 64, 16, 4, 4, false, 2>(c, "general");
   const bool small_inst = p.k > 0 && p.m <= 64 && p.n <= 64 && (p.batch > 1 || p.k <= 4096);
-  if (!small_inst && !(c.flags & TB_FLAG_SIMT_GENERAL)) {
-    const int rc = dispatch_sgemm_tma(c);
+  if (!small_inst && want_tma) {
+    const int rc = dispatch_sgemm_tma(c, tma_tile);
     if (rc >= 0) return rc;
   }
   // Small instances: persistent cp.async-pipelined kernel (bitwise identical).
@@ -411,8 +421,8 @@ int dispatch_sgemm(const Call& c) {
     // tensor maps over the batch) when the operands allow tensor maps; else
     // the register-staged tiled kernel with a 4x8 micro-tile (measured faster
     // than the cp.async small kernel for 64^3, tools/sgemm_batched_variants.cu)
-    if (!(c.flags & TB_FLAG_SIMT_GENERAL)) {
-      const int rc = dispatch_sgemm_tma(c);
+    if (want_tma) {
+      const int rc = dispatch_sgemm_tma(c, 2);
       if (rc >= 0) return rc;
     }
     return launch_simt<64, 64, 16, 4, 8, true, 2>(c, "64x64 4x8");

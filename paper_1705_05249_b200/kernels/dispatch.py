@@ -45,6 +45,14 @@ def require_gpu(ctx: Context) -> None:
 _PARAM_STRUCTS: dict = {}
 
 
+def native_config(config: Configuration, source: str) -> Configuration | None:
+    """The configuration the native dispatcher sees: None for the built-in
+    default (the library then picks tiles by shape, from measured crossovers),
+    the configuration itself when it came from an override or the tuning DB
+    (its MWG / NWG / KWG / VW* then select the kernel)."""
+    return None if source == "builtin" else config
+
+
 def _params(config: Configuration | None):
     if config is None:
         return None

@@ -24,7 +24,7 @@ import numpy as np
 from ..core import Buffer, Context, Layout, Precision, Transpose, matrix_span
 from ..errors import UsageError
 from ..kernels import native
-from ..kernels.dispatch import gemm_batched_native, gemm_strided_batched_native, prec_code
+from ..kernels.dispatch import gemm_batched_native, gemm_strided_batched_native, native_config, prec_code
 from ..kernels.engine import WorkGrid, pre_launch, record_launch, reference_grid
 from .common import check_precision, get_store, scalars, stored_dims
 from .level3 import route_family
@@ -116,10 +116,10 @@ def _validate(ctx, layout, trans_a, trans_b, m, n, k, a, a_offs, lda, b, b_offs,
 
 def _launch_family(ctx, precision, m, n, k):
     store = get_store(ctx)
-    cfg, _ = store.resolve("gemm", precision, ctx.device, (m, n, k))
+    cfg, source = store.resolve("gemm", precision, ctx.device, (m, n, k))
     route = route_family(m, n, k, store.direct_threshold, None)
     family = "gemm_direct" if route == "direct" else "gemm"
-    return cfg, family
+    return cfg, family, native_config(cfg, source)
 
 
 def gemm_batched(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Transpose,
@@ -143,14 +143,14 @@ def gemm_batched(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Tran
     _check_no_overlap(c_offs, c_span, "gemm output")
     if m == 0 or n == 0:
         return
-    cfg, family = _launch_family(ctx, precision, m, n, k)
+    cfg, family, ncfg = _launch_family(ctx, precision, m, n, k)
     grid1 = reference_grid(family, m, n, cfg)
     grid = WorkGrid((batch_count,) + grid1.work_groups, grid1.work_group_size)
     computes = k != 0 and bool(np.any(al != 0))
     if computes:
         pre_launch(ctx, family, cfg, grid, precision)
     launched = gemm_batched_native(ctx, precision, layout, trans_a, trans_b, m, n, k, al,
-                                   a, a_offs, lda, b, b_offs, ldb, be, c, c_offs, ldc, cfg)
+                                   a, a_offs, lda, b, b_offs, ldb, be, c, c_offs, ldc, ncfg)
     if computes:
         # All-alpha-zero batches make no launch in the reference
         # (extras.py:281-286), so last_launch is left unchanged then.
@@ -192,7 +192,7 @@ def gemm_strided_batched(ctx: Context, layout: Layout, trans_a: Transpose, trans
     # never overlap (extras.py:116-122 would find no pair).
     if m == 0 or n == 0:
         return
-    cfg, family = _launch_family(ctx, precision, m, n, k)
+    cfg, family, ncfg = _launch_family(ctx, precision, m, n, k)
     grid1 = reference_grid(family, m, n, cfg)
     grid = WorkGrid((batch_count,) + grid1.work_groups, grid1.work_group_size)
     computes = k != 0 and al != 0
@@ -201,6 +201,6 @@ def gemm_strided_batched(ctx: Context, layout: Layout, trans_a: Transpose, trans
     launched = gemm_strided_batched_native(
         ctx, precision, layout, trans_a, trans_b, m, n, k, float(al),
         a, a_offset, lda_e, stride_a, b, b_offset, ldb_e, stride_b, float(be),
-        c, c_offset, ldc_e, stride_c, batch_count, cfg, native.FLAG_TF32 if tf32 else 0)
+        c, c_offset, ldc_e, stride_c, batch_count, ncfg, native.FLAG_TF32 if tf32 else 0)
     if computes:
         record_launch(ctx, family, cfg, grid, launched)

@@ -1,5 +1,5 @@
 """On-device tuning of the BASELINE C3 shapes + the problem-specific-tuning
-heat map (paper Fig. 4) on the B200.  Writes profiles/r1_tuning_db.json and
+heat map (paper Fig. 4) on the B200.  Writes gpurun_out/r1_tuning_db.json and
 profiles/r1_heatmap_*.json.  Dev tool; uses only the public API."""
 import json, sys, time
 sys.path.insert(0, '.')
@@ -32,10 +32,10 @@ for prec in (tb.Precision.H, tb.Precision.S):
                    seconds=time.perf_counter() - t0)
         summary.append(row)
         print(json.dumps({k_: v for k_, v in row.items() if k_ != "best"}), flush=True)
-db.save("profiles/r1_tuning_db.json")
-json.dump(summary, open("profiles/r1_tuning_summary.json", "w"), indent=1)
+db.save("gpurun_out/r1_tuning_db.json")
+json.dump(summary, open("gpurun_out/r1_tuning_summary.json", "w"), indent=1)
 for prec in (tb.Precision.S, tb.Precision.H):
     res = tb.heatmap_experiment([(64, 3136, 576), (4096, 128, 9216), (1024, 1024, 1024)], prec, ctx,
                                 budget=8, seed=5, runs=5)
-    json.dump(res.to_json(), open(f"profiles/r1_heatmap_{prec.value}.json", "w"), indent=1)
+    json.dump(res.to_json(), open(f"gpurun_out/r1_heatmap_{prec.value}.json", "w"), indent=1)
     print(prec.value, "heatmap %", np.round(res.relative_perf, 1).tolist(), flush=True)
