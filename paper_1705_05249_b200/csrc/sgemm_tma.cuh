@@ -41,11 +41,15 @@ struct TmaSgemmCfg {
   static constexpr int NT = TY * TX;
   static constexpr int NW = NT / 32;
   static constexpr int QM = TM / 4, QN = TN / 4;
-  static constexpr bool PAIR_N = !A_MN;
+  // both operands K-contiguous: A is transposed in shared memory once per
+  // stage ([BM][32] -> [32][BM], double-buffered) and then read like an
+  // M-contiguous A
+  static constexpr bool A_T = !A_MN && !B_MN;
+  static constexpr bool PAIR_N = !A_MN && !A_T;
   static constexpr int A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-  static_assert(A_MN || B_MN, "both K-contiguous: use sgemm_simt.cuh");
+  static constexpr int T_BYTES = A_T ? 2 * A_BYTES : 0;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + T_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(BK == 32, "K-contiguous tiles are 128-byte SWIZZLE_128B rows");
   static_assert(TM % 4 == 0 && TN % 4 == 0 && NT % 32 == 0, "tile shape");
   static_assert(A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0, "1024-byte aligned stage tiles");
@@ -70,7 +74,8 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
   constexpr bool PN = Cfg::PAIR_N;
   extern __shared__ __align__(1024) uint8_t tma_smem_raw[];
   uint8_t* smem = smem_align1024(tma_smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  float* a_t = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES);  // A_T buffers
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::T_BYTES);
   uint64_t* empty = full + STAGES;
 
   const int tid = threadIdx.x;
@@ -135,7 +140,8 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
   //   K  operand: (j*T + t)*BK + ((k4 ^ ((j*T + t) & 7)) * 4)
   const int a_sw = ty & 7;  // (j*TY + ty) & 7 == ty & 7 when TY % 8 == 0
   const int b_sw = tx & 7;
-  static_assert(A_MN || Cfg::TY % 8 == 0, "A swizzle phase per thread");
+  static_assert(A_MN || Cfg::A_T || Cfg::TY % 8 == 0, "A swizzle phase per thread");
+  constexpr bool A_FRAG_MN = A_MN || Cfg::A_T;  // A fragments read from an M-contiguous tile
   static_assert(B_MN || Cfg::TX % 8 == 0, "B swizzle phase per thread");
 
   for (int kt = 0; kt < ktiles; ++kt) {
@@ -150,6 +156,24 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
     }
     mbar_wait(&full[s], ph);
     const float* sa = reinterpret_cast<const float*>(smem + s * Cfg::STAGE_BYTES);
+    if constexpr (Cfg::A_T) {
+      // [BM][32] SWIZZLE_128B -> [32][BM]: lanes take consecutive rows of one
+      // 16-byte chunk column (8-row groups cover all banks on the read, the
+      // 4 scalar writes per chunk are unit-stride across the warp)
+      float* dst = a_t + (kt & 1) * (BM * BK);
+#pragma unroll
+      for (int j = 0; j < BM * (BK / 4) / Cfg::NT; ++j) {
+        const int e = tid + j * Cfg::NT;
+        const int r = e % BM, c = e / BM;
+        const float4 v = *reinterpret_cast<const float4*>(sa + r * BK + ((c ^ (r & 7)) * 4));
+        dst[(4 * c + 0) * BM + r] = v.x;
+        dst[(4 * c + 1) * BM + r] = v.y;
+        dst[(4 * c + 2) * BM + r] = v.z;
+        dst[(4 * c + 3) * BM + r] = v.w;
+      }
+      __syncthreads();
+      sa = dst;
+    }
     const float* sb = reinterpret_cast<const float*>(smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES);
     const int kcur = min(k_total - kt * BK, BK);
 
@@ -175,8 +199,8 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
     if (kcur == BK) {
 #pragma unroll
       for (int k4 = 0; k4 < BK / 4; ++k4) {
-        float4 aq[A_MN ? 1 : TM], bq[B_MN ? 1 : TN];
-        if constexpr (!A_MN) {
+        float4 aq[A_FRAG_MN ? 1 : TM], bq[B_MN ? 1 : TN];
+        if constexpr (!A_FRAG_MN) {
 #pragma unroll
           for (int i = 0; i < TM; ++i)
             aq[i] = *reinterpret_cast<const float4*>(sa + (i * Cfg::TY + ty) * BK + ((k4 ^ a_sw) * 4));
@@ -190,7 +214,7 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
         for (int k1 = 0; k1 < 4; ++k1) {
           const int kk = k4 * 4 + k1;
           float af[TM], bf[TN];
-          if constexpr (A_MN) {
+          if constexpr (A_FRAG_MN) {
             load_a_mn(kk, af);
           } else {
 #pragma unroll
@@ -210,7 +234,7 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
 #pragma unroll 1
       for (int kk = 0; kk < kcur; ++kk) {
         float af[TM], bf[TN];
-        if constexpr (A_MN) {
+        if constexpr (A_FRAG_MN) {
           load_a_mn(kk, af);
         } else {
 #pragma unroll
@@ -245,7 +269,7 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
     if constexpr (B_MN) return (j / 4) * (BN / Cfg::QN) + tx * 4 + (j % 4);
     else return j * Cfg::TX + tx;
   };
-  if constexpr (A_MN) {
+  if constexpr (A_FRAG_MN) {
     // rows q*(BM/QM) + ty*4 + r: 4 consecutive rows per 128-bit store
     const bool cvec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((p.ldc & 3) == 0);
 #pragma unroll

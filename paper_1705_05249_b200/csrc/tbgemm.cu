@@ -247,7 +247,6 @@ int launch_stma(const Call& c) {
 int dispatch_sgemm_tma(const Call& c, int tile) {
   const Problem& p = c.p;
   const bool amn = !p.a_kcontig, bmn = p.b_ncontig;
-  if (!amn && !bmn) return -1;  // both K-contiguous: FFMA2 pairs would need register shuffles
   if (p.a_offs || p.b_offs || p.alphas || p.betas || p.k <= 0 || p.alpha == 0.0f) return -1;
   if ((p.lda % 4) || (p.ldb % 4) || !aligned_elems(p.a, p.a_off, 4, 16) || !aligned_elems(p.b, p.b_off, 4, 16))
     return -1;
@@ -264,11 +263,13 @@ int dispatch_sgemm_tma(const Call& c, int tile) {
   if (big && !one_tile) {
     if (amn && bmn) return launch_stma<64, 128, 8, 8, 4, true, true>(c);
     if (amn) return launch_stma<128, 128, 16, 8, 2, true, false>(c);
-    return launch_stma<128, 128, 8, 16, 2, false, true>(c);
+    if (bmn) return launch_stma<128, 128, 8, 16, 2, false, true>(c);
+    return launch_stma<128, 128, 16, 8, 2, false, false>(c);  // A transposed in shared memory
   }
   if (amn && bmn) return launch_stma<64, 64, 4, 8, 3, true, true>(c);
   if (amn) return launch_stma<64, 64, 4, 8, 3, true, false>(c);
-  return launch_stma<64, 64, 8, 4, 4, false, true>(c);
+  if (bmn) return launch_stma<64, 64, 8, 4, 4, false, true>(c);
+  return launch_stma<64, 64, 4, 8, 3, false, false>(c);
 }
 
 template <int MI, int NI, int TM, int TN, bool AK, bool BNC>

@@ -63,7 +63,7 @@ def test_big_tiles_bitwise(ctx, layout, ta, tbn):
     m, n, k = 3072, 3200, 77   # ld of 77 padded to 80
     got, want, kern = _run(ctx, layout, ta, tbn, m, n, k, 1.25, -0.75, 11)
     assert got.tobytes() == want.tobytes()
-    assert kern.startswith("sgemm_simt" if _canonical_is_both_k(layout, ta, tbn) else "sgemm_tma_"), kern
+    assert kern.startswith("sgemm_tma_"), kern
 
 
 @pytest.mark.parametrize("layout", ["col", "row"])
@@ -74,8 +74,9 @@ def test_mid_tiles_ragged_bitwise(ctx, layout, ta, tbn, shape):
     m, n, k = shape
     got, want, kern = _run(ctx, layout, ta, tbn, m, n, k, 0.5, 2.0, sum(shape))
     assert got.tobytes() == want.tobytes(), kern
-    if not _canonical_is_both_k(layout, ta, tbn):
-        assert kern.startswith("sgemm_tma_"), kern
+    assert kern.startswith("sgemm_tma_"), kern
+    # both operands K-contiguous: A goes through the shared-memory transpose
+    assert kern.endswith("_kk") == _canonical_is_both_k(layout, ta, tbn), kern
 
 
 def test_padded_leading_dims_and_beta_zero(ctx):

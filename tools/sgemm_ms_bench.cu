@@ -87,8 +87,7 @@ template <int BM, int BN, int TM, int TN, int ST, int MINB, bool AK, bool BNC>
 void run_tma(Problem p, const char* name) {
   if (g_only && !strstr(name, g_only)) return;
   constexpr bool AMN = !AK, BMN = BNC;
-  if constexpr (!AMN && !BMN) return;
-  else {
+  {
     using Cfg = TmaSgemmCfg<BM, BN, 32, TM, TN, ST, AMN, BMN>;
     CUtensorMap ta, tbm;
     if (AMN) mk(&ta, p.a, p.m, p.k, p.lda, BM, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
@@ -105,16 +104,17 @@ void run_tma(Problem p, const char* name) {
 
 template <bool AK, bool BNC>
 void suite(Problem p) {
+  run_simt<128, 256, 8, 8, 16, 1, AK, BNC>(p, "simt 128x256x8 8x16");
   if constexpr (!AK) {
     run_tma<128, 128, 16, 8, 2, 2, AK, BNC>(p, "tma 128x128x32 16x8 st2 (128t)");
-    run_tma<64, 64, 4, 8, 4, 2, AK, BNC>(p, "tma 64x64x32 4x8 st4 (128t)");
     run_tma<64, 64, 4, 8, 3, 2, AK, BNC>(p, "tma 64x64x32 4x8 st3 (128t)");
-    run_tma<64, 64, 4, 8, 6, 2, AK, BNC>(p, "tma 64x64x32 4x8 st6 (128t)");
-    run_tma<64, 128, 8, 8, 4, 2, AK, BNC>(p, "tma 64x128x32 8x8 st4 (128t)");
-  } else {
+  } else if constexpr (BNC) {
     run_tma<128, 128, 8, 16, 2, 2, AK, BNC>(p, "tma 128x128x32 8x16 st2 (128t)");
     run_tma<64, 64, 8, 4, 4, 2, AK, BNC>(p, "tma 64x64x32 8x4 st4 (128t)");
-    run_tma<64, 64, 8, 4, 6, 2, AK, BNC>(p, "tma 64x64x32 8x4 st6 (128t)");
+  } else {
+    run_tma<128, 128, 16, 8, 2, 2, AK, BNC>(p, "tmaT 128x128x32 16x8 st2 (128t)");
+    run_tma<128, 128, 16, 8, 3, 2, AK, BNC>(p, "tmaT 128x128x32 16x8 st3 (128t)");
+    run_tma<64, 64, 4, 8, 3, 2, AK, BNC>(p, "tmaT 64x64x32 4x8 st3 (128t)");
   }
 }
 
