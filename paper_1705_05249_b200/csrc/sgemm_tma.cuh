@@ -31,11 +31,13 @@
 // operands use the register-staged kernel, sgemm_simt.cuh).
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace tb {
 
-template <int BM, int BN, int BK, int TM, int TN, int STAGES, bool A_MN, bool B_MN>
+template <int BM, int BN, int BK, int TM, int TN, int STAGES, bool A_MN, bool B_MN, bool XP = false>
 struct TmaSgemmCfg {
   static constexpr int TY = BM / TM, TX = BN / TN;
   static constexpr int NT = TY * TX;
@@ -44,11 +46,13 @@ struct TmaSgemmCfg {
   // both operands K-contiguous: A is transposed in shared memory once per
   // stage ([BM][32] -> [32][BM], double-buffered) and then read like an
   // M-contiguous A
-  static constexpr bool A_T = !A_MN && !B_MN;
+  // XP: transpose every K-contiguous operand the same way (B too)
+  static constexpr bool A_T = !A_MN && (!B_MN || XP);
+  static constexpr bool B_T = !B_MN && XP;
   static constexpr bool PAIR_N = !A_MN && !A_T;
   static constexpr int A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int T_BYTES = A_T ? 2 * A_BYTES : 0;
+  static constexpr int T_BYTES = (A_T ? 2 * A_BYTES : 0) + (B_T ? 2 * B_BYTES : 0);
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + T_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(BK == 32, "K-contiguous tiles are 128-byte SWIZZLE_128B rows");
   static_assert(TM % 4 == 0 && TN % 4 == 0 && NT % 32 == 0, "tile shape");
@@ -66,15 +70,16 @@ __device__ __forceinline__ void outer_ffma2_n(float2 (&acc2)[TM][TN / 2], const 
                                acc2[i][j2]);
 }
 
-template <int BM, int BN, int BK, int TM, int TN, int STAGES, bool A_MN, bool B_MN, int MINB>
-__global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, B_MN>::NT, MINB)
+template <int BM, int BN, int BK, int TM, int TN, int STAGES, bool A_MN, bool B_MN, int MINB, bool XP = false>
+__global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, B_MN, XP>::NT, MINB)
     sgemm_tma_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                      Problem p, int tiles_m, int tiles_n, int group_m) {
-  using Cfg = TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, B_MN>;
+  using Cfg = TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, B_MN, XP>;
   constexpr bool PN = Cfg::PAIR_N;
   extern __shared__ __align__(1024) uint8_t tma_smem_raw[];
   uint8_t* smem = smem_align1024(tma_smem_raw);
   float* a_t = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES);  // A_T buffers
+  float* b_t = a_t + (Cfg::A_T ? 2 * BM * BK : 0);                            // B_T buffers
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::T_BYTES);
   uint64_t* empty = full + STAGES;
 
@@ -142,7 +147,8 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
   const int b_sw = tx & 7;
   static_assert(A_MN || Cfg::A_T || Cfg::TY % 8 == 0, "A swizzle phase per thread");
   constexpr bool A_FRAG_MN = A_MN || Cfg::A_T;  // A fragments read from an M-contiguous tile
-  static_assert(B_MN || Cfg::TX % 8 == 0, "B swizzle phase per thread");
+  static_assert(B_MN || Cfg::B_T || Cfg::TX % 8 == 0, "B swizzle phase per thread");
+  constexpr bool B_FRAG_MN = B_MN || Cfg::B_T;
 
   for (int kt = 0; kt < ktiles; ++kt) {
     const int s = kt % STAGES;
@@ -156,25 +162,36 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
     }
     mbar_wait(&full[s], ph);
     const float* sa = reinterpret_cast<const float*>(smem + s * Cfg::STAGE_BYTES);
-    if constexpr (Cfg::A_T) {
-      // [BM][32] SWIZZLE_128B -> [32][BM]: lanes take consecutive rows of one
-      // 16-byte chunk column (8-row groups cover all banks on the read, the
-      // 4 scalar writes per chunk are unit-stride across the warp)
-      float* dst = a_t + (kt & 1) * (BM * BK);
+    const float* sb = reinterpret_cast<const float*>(smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES);
+    if constexpr (Cfg::A_T || Cfg::B_T) {
+      // [ROWS][32] SWIZZLE_128B -> [32][ROWS]: lanes take consecutive rows of
+      // one 16-byte chunk column (8-row groups cover all banks on the read,
+      // the 4 scalar writes per chunk are unit-stride across the warp)
+      auto xpose = [&](const float* src, float* dst, auto rows_c) {
+        constexpr int ROWS = decltype(rows_c)::value;
 #pragma unroll
-      for (int j = 0; j < BM * (BK / 4) / Cfg::NT; ++j) {
-        const int e = tid + j * Cfg::NT;
-        const int r = e % BM, c = e / BM;
-        const float4 v = *reinterpret_cast<const float4*>(sa + r * BK + ((c ^ (r & 7)) * 4));
-        dst[(4 * c + 0) * BM + r] = v.x;
-        dst[(4 * c + 1) * BM + r] = v.y;
-        dst[(4 * c + 2) * BM + r] = v.z;
-        dst[(4 * c + 3) * BM + r] = v.w;
+        for (int j = 0; j < ROWS * (BK / 4) / Cfg::NT; ++j) {
+          const int e = tid + j * Cfg::NT;
+          const int r = e % ROWS, c = e / ROWS;
+          const float4 v = *reinterpret_cast<const float4*>(src + r * BK + ((c ^ (r & 7)) * 4));
+          dst[(4 * c + 0) * ROWS + r] = v.x;
+          dst[(4 * c + 1) * ROWS + r] = v.y;
+          dst[(4 * c + 2) * ROWS + r] = v.z;
+          dst[(4 * c + 3) * ROWS + r] = v.w;
+        }
+      };
+      if constexpr (Cfg::A_T) {
+        float* dst = a_t + (kt & 1) * (BM * BK);
+        xpose(sa, dst, std::integral_constant<int, BM>{});
+        sa = dst;
+      }
+      if constexpr (Cfg::B_T) {
+        float* dst = b_t + (kt & 1) * (BN * BK);
+        xpose(sb, dst, std::integral_constant<int, BN>{});
+        sb = dst;
       }
       __syncthreads();
-      sa = dst;
     }
-    const float* sb = reinterpret_cast<const float*>(smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES);
     const int kcur = min(k_total - kt * BK, BK);
 
     auto step = [&](const float (&af)[TM], const float (&bf)[TN]) {
@@ -199,13 +216,13 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
     if (kcur == BK) {
 #pragma unroll
       for (int k4 = 0; k4 < BK / 4; ++k4) {
-        float4 aq[A_FRAG_MN ? 1 : TM], bq[B_MN ? 1 : TN];
+        float4 aq[A_FRAG_MN ? 1 : TM], bq[B_FRAG_MN ? 1 : TN];
         if constexpr (!A_FRAG_MN) {
 #pragma unroll
           for (int i = 0; i < TM; ++i)
             aq[i] = *reinterpret_cast<const float4*>(sa + (i * Cfg::TY + ty) * BK + ((k4 ^ a_sw) * 4));
         }
-        if constexpr (!B_MN) {
+        if constexpr (!B_FRAG_MN) {
 #pragma unroll
           for (int j = 0; j < TN; ++j)
             bq[j] = *reinterpret_cast<const float4*>(sb + (j * Cfg::TX + tx) * BK + ((k4 ^ b_sw) * 4));
@@ -220,7 +237,7 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
 #pragma unroll
             for (int i = 0; i < TM; ++i) af[i] = k1 == 0 ? aq[i].x : k1 == 1 ? aq[i].y : k1 == 2 ? aq[i].z : aq[i].w;
           }
-          if constexpr (B_MN) {
+          if constexpr (B_FRAG_MN) {
             load_b_mn(kk, bf);
           } else {
 #pragma unroll
@@ -241,7 +258,7 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
           for (int i = 0; i < TM; ++i)
             af[i] = sa[(i * Cfg::TY + ty) * BK + (((kk >> 2) ^ a_sw) * 4) + (kk & 3)];
         }
-        if constexpr (B_MN) {
+        if constexpr (B_FRAG_MN) {
           load_b_mn(kk, bf);
         } else {
 #pragma unroll
@@ -266,7 +283,7 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
     else return (i & 1) ? acc2[i >> 1][j].y : acc2[i >> 1][j].x;
   };
   auto col_of = [&](int j) -> int {
-    if constexpr (B_MN) return (j / 4) * (BN / Cfg::QN) + tx * 4 + (j % 4);
+    if constexpr (B_FRAG_MN) return (j / 4) * (BN / Cfg::QN) + tx * 4 + (j % 4);
     else return j * Cfg::TX + tx;
   };
   if constexpr (A_FRAG_MN) {

@@ -83,19 +83,19 @@ static void mk(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint6
   if (r) printf("encode failed %d\n", (int)r);
 }
 
-template <int BM, int BN, int TM, int TN, int ST, int MINB, bool AK, bool BNC>
+template <int BM, int BN, int TM, int TN, int ST, int MINB, bool AK, bool BNC, bool XP = false>
 void run_tma(Problem p, const char* name) {
   if (g_only && !strstr(name, g_only)) return;
   constexpr bool AMN = !AK, BMN = BNC;
   {
-    using Cfg = TmaSgemmCfg<BM, BN, 32, TM, TN, ST, AMN, BMN>;
+    using Cfg = TmaSgemmCfg<BM, BN, 32, TM, TN, ST, AMN, BMN, XP>;
     CUtensorMap ta, tbm;
     if (AMN) mk(&ta, p.a, p.m, p.k, p.lda, BM, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
     else mk(&ta, p.a, p.k, p.m, p.lda, 32, BM, CU_TENSOR_MAP_SWIZZLE_128B);
     if (BMN) mk(&tbm, p.b, p.n, p.k, p.ldb, BN, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
     else mk(&tbm, p.b, p.k, p.n, p.ldb, 32, BN, CU_TENSOR_MAP_SWIZZLE_128B);
     const int tm = (p.m + BM - 1) / BM, tn = (p.n + BN - 1) / BN;
-    auto k = sgemm_tma_kernel<BM, BN, 32, TM, TN, ST, AMN, BMN, MINB>;
+    auto k = sgemm_tma_kernel<BM, BN, 32, TM, TN, ST, AMN, BMN, MINB, XP>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     float ms = time_it([&] { k<<<tm * tn, Cfg::NT, Cfg::SMEM_BYTES>>>(ta, tbm, p, tm, tn, 8); });
     report(name, ms, p);
@@ -104,17 +104,28 @@ void run_tma(Problem p, const char* name) {
 
 template <bool AK, bool BNC>
 void suite(Problem p) {
-  run_simt<128, 256, 8, 8, 16, 1, AK, BNC>(p, "simt 128x256x8 8x16");
-  if constexpr (!AK) {
-    run_tma<128, 128, 16, 8, 2, 2, AK, BNC>(p, "tma 128x128x32 16x8 st2 (128t)");
-    run_tma<64, 64, 4, 8, 3, 2, AK, BNC>(p, "tma 64x64x32 4x8 st3 (128t)");
+  if constexpr (!AK && BNC) {
+    run_tma<128, 128, 16, 8, 2, 2, AK, BNC>(p, "tma 128x128x32 16x8 st2");
+    run_tma<64, 128, 8, 8, 4, 2, AK, BNC>(p, "tma 64x128x32 8x8 st4");
+  } else if constexpr (!AK) {
+    run_tma<128, 128, 16, 8, 2, 2, AK, BNC>(p, "tma 128x128x32 16x8 st2");
+    run_tma<128, 128, 16, 8, 2, 2, AK, BNC, true>(p, "XP 128x128x32 16x8 st2");
+    run_tma<64, 128, 8, 8, 2, 2, AK, BNC, true>(p, "XP 64x128x32 8x8 st2");
+    run_tma<64, 128, 8, 8, 3, 2, AK, BNC, true>(p, "XP 64x128x32 8x8 st3");
+    run_tma<64, 64, 4, 8, 3, 2, AK, BNC>(p, "tma 64x64x32 4x8 st3");
+    run_tma<64, 64, 4, 8, 3, 2, AK, BNC, true>(p, "XP 64x64x32 4x8 st3");
   } else if constexpr (BNC) {
-    run_tma<128, 128, 8, 16, 2, 2, AK, BNC>(p, "tma 128x128x32 8x16 st2 (128t)");
-    run_tma<64, 64, 8, 4, 4, 2, AK, BNC>(p, "tma 64x64x32 8x4 st4 (128t)");
+    run_tma<128, 128, 8, 16, 2, 2, AK, BNC>(p, "tma 128x128x32 8x16 st2");
+    run_tma<128, 128, 16, 8, 2, 2, AK, BNC, true>(p, "XP 128x128x32 16x8 st2");
+    run_tma<64, 128, 8, 8, 2, 2, AK, BNC, true>(p, "XP 64x128x32 8x8 st2");
+    run_tma<64, 64, 8, 4, 4, 2, AK, BNC>(p, "tma 64x64x32 8x4 st4");
+    run_tma<64, 64, 4, 8, 3, 2, AK, BNC, true>(p, "XP 64x64x32 4x8 st3");
   } else {
-    run_tma<128, 128, 16, 8, 2, 2, AK, BNC>(p, "tmaT 128x128x32 16x8 st2 (128t)");
-    run_tma<128, 128, 16, 8, 3, 2, AK, BNC>(p, "tmaT 128x128x32 16x8 st3 (128t)");
-    run_tma<64, 64, 4, 8, 3, 2, AK, BNC>(p, "tmaT 64x64x32 4x8 st3 (128t)");
+    run_tma<128, 128, 16, 8, 2, 2, AK, BNC>(p, "tmaT 128x128x32 16x8 st2");
+    run_tma<128, 128, 16, 8, 2, 1, AK, BNC, true>(p, "XP 128x128x32 16x8 st2");
+    run_tma<64, 128, 8, 8, 2, 2, AK, BNC, true>(p, "XP 64x128x32 8x8 st2");
+    run_tma<64, 64, 4, 8, 3, 2, AK, BNC>(p, "tmaT 64x64x32 4x8 st3");
+    run_tma<64, 64, 4, 8, 3, 2, AK, BNC, true>(p, "XP 64x64x32 4x8 st3");
   }
 }
 
