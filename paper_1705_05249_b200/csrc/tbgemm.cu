@@ -259,6 +259,13 @@ int dispatch_sgemm_tma(const Call& c, int tile) {
   // tiles the big tiles win (64x128 8x8 when both operands are M/N-contiguous:
   // 66 TFLOP/s at 8192^3); below that 64x64 tiles of 4x8 (8x4) micro-tiles
   // keep every SM busy (1024^3 37.6, C3 (4096,128,9216) 34.8 TFLOP/s).
+  if (tile == 3) {
+    // batched instances of at most 32x32: one 32x32 tile each, 64 threads of 4x4
+    if (amn && bmn) return launch_stma<32, 32, 4, 4, 2, true, true>(c);
+    if (amn) return launch_stma<32, 32, 4, 4, 2, true, false>(c);
+    if (bmn) return launch_stma<32, 32, 4, 4, 2, false, true, true>(c);
+    return launch_stma<32, 32, 4, 4, 2, false, false, true>(c);
+  }
   const bool one_tile = p.m <= 64 && p.n <= 64;  // batched small instances: one 64x64 tile each
   const bool big = tile == 0 ? tiles128 >= 4 * sms : tile == 1;
   if (big && !one_tile) {
@@ -421,7 +428,16 @@ int dispatch_sgemm(const Call& c) {
   }
   // Small instances: persistent cp.async-pipelined kernel (bitwise identical).
   if (p.k > 0 && p.m <= 64 && p.n <= 64 && (p.batch > 1 || p.k <= 4096)) {
-    if (p.m <= 32 && p.n <= 32) return launch_ss_layout<32, 32, 4, 4>(c);
+    if (p.m <= 32 && p.n <= 32) {
+      // one 32x32 tile per instance on the TMA kernel when the operands allow
+      // tensor maps (S32 batched 59.4 -> 48.7 us; a persistent variant of the
+      // TMA kernel measured slower: 53.6 us, and 20 % slower at 8192^3)
+      if (want_tma) {
+        const int rc = dispatch_sgemm_tma(c, 3);
+        if (rc >= 0) return rc;
+      }
+      return launch_ss_layout<32, 32, 4, 4>(c);
+    }
     // 33..64: one 64x64 tile per instance on the TMA-fed FFMA2 kernel (3-D
     // tensor maps over the batch) when the operands allow tensor maps; else
     // the register-staged tiled kernel with a 4x8 micro-tile (measured faster

@@ -175,8 +175,8 @@ def test_full_size_batch_16384(ctx, prec, size):
 @pytest.mark.parametrize("tbt", [Transpose.NO, Transpose.YES])
 @pytest.mark.parametrize("shape", [(32, 32, 32), (64, 64, 64), (20, 50, 77), (64, 17, 300), (8, 64, 1)])
 def test_small_path_bitwise_equals_general_path(ctx, prec, layout, ta, tbt, shape):
-    """The packed small-instance kernels (tcgen05 for H, cp.async FFMA for S)
-    give the same bits as the general kernels forced via flags."""
+    """The small-instance kernels (packed tcgen05 for H, TMA-fed FFMA2 tiles
+    for S) give the same bits as the general kernels forced via flags."""
     from paper_1705_05249_b200.kernels import native
     from paper_1705_05249_b200.kernels.dispatch import gemm_strided_batched_native
 
@@ -199,9 +199,11 @@ def test_small_path_bitwise_equals_general_path(ctx, prec, layout, ta, tbt, shap
     assert "small" not in kernels[1], kernels
     aligned = (prec is Precision.S and all(v % 4 == 0 for v in (ea, eb, lda, ldb))) or \
         (prec is Precision.H and all(v % 8 == 0 for v in (ea, eb, lda, ldb)))
-    small_expected = prec is Precision.H or (aligned and m <= 32 and n <= 32)
-    if small_expected:
+    if prec is Precision.H:
         assert "small" in kernels[0], kernels
+    elif aligned and m <= 32 and n <= 32:
+        # strided S batches of <= 32x32 instances: one TMA-fed 32x32 tile each
+        assert kernels[0].startswith("sgemm_tma_32x32"), kernels
     assert outs[0].tobytes() == outs[1].tobytes(), kernels
 
 
