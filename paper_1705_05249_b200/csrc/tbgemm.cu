@@ -277,6 +277,15 @@ int dispatch_sgemm_tma(const Call& c, int tile) {
     if (bmn) return launch_stma<64, 128, 8, 8, 2, false, true, true>(c);
     return launch_stma<64, 128, 8, 8, 2, false, false, true>(c);
   }
+  // fewer 64x64 tiles than SMs (e.g. C3 (64, 3136, 576): 49 tiles): 64x32
+  // tiles of 4x4 (21 -> 14 us there; tools/sgemm_ms_bench.cu)
+  const int64_t tiles64 = ((p.m + 63) / 64) * ((p.n + 63) / 64) * p.batch;
+  if (tile == 0 && tiles64 < sms) {
+    if (amn && bmn) return launch_stma<64, 32, 4, 4, 3, true, true>(c);
+    if (amn) return launch_stma<64, 32, 4, 4, 3, true, false>(c);
+    if (bmn) return launch_stma<64, 32, 4, 4, 3, false, true>(c);
+    return launch_stma<64, 32, 4, 4, 3, false, false>(c);
+  }
   if (amn && bmn) return launch_stma<64, 64, 4, 8, 3, true, true>(c);
   if (amn) return launch_stma<64, 64, 4, 8, 3, true, false>(c);
   if (bmn) return launch_stma<64, 64, 8, 4, 4, false, true>(c);

@@ -104,28 +104,14 @@ void run_tma(Problem p, const char* name) {
 
 template <bool AK, bool BNC>
 void suite(Problem p) {
-  if constexpr (!AK && BNC) {
-    run_tma<128, 128, 16, 8, 2, 2, AK, BNC>(p, "tma 128x128x32 16x8 st2");
-    run_tma<64, 128, 8, 8, 4, 2, AK, BNC>(p, "tma 64x128x32 8x8 st4");
-  } else if constexpr (!AK) {
-    run_tma<128, 128, 16, 8, 2, 2, AK, BNC>(p, "tma 128x128x32 16x8 st2");
-    run_tma<128, 128, 16, 8, 2, 2, AK, BNC, true>(p, "XP 128x128x32 16x8 st2");
-    run_tma<64, 128, 8, 8, 2, 2, AK, BNC, true>(p, "XP 64x128x32 8x8 st2");
-    run_tma<64, 128, 8, 8, 3, 2, AK, BNC, true>(p, "XP 64x128x32 8x8 st3");
+  if constexpr (!AK && !BNC) {
     run_tma<64, 64, 4, 8, 3, 2, AK, BNC>(p, "tma 64x64x32 4x8 st3");
-    run_tma<64, 64, 4, 8, 3, 2, AK, BNC, true>(p, "XP 64x64x32 4x8 st3");
-  } else if constexpr (BNC) {
-    run_tma<128, 128, 8, 16, 2, 2, AK, BNC>(p, "tma 128x128x32 8x16 st2");
-    run_tma<128, 128, 16, 8, 2, 2, AK, BNC, true>(p, "XP 128x128x32 16x8 st2");
-    run_tma<64, 128, 8, 8, 2, 2, AK, BNC, true>(p, "XP 64x128x32 8x8 st2");
-    run_tma<64, 64, 8, 4, 4, 2, AK, BNC>(p, "tma 64x64x32 8x4 st4");
-    run_tma<64, 64, 4, 8, 3, 2, AK, BNC, true>(p, "XP 64x64x32 4x8 st3");
-  } else {
-    run_tma<128, 128, 16, 8, 2, 2, AK, BNC>(p, "tmaT 128x128x32 16x8 st2");
-    run_tma<128, 128, 16, 8, 2, 1, AK, BNC, true>(p, "XP 128x128x32 16x8 st2");
-    run_tma<64, 128, 8, 8, 2, 2, AK, BNC, true>(p, "XP 64x128x32 8x8 st2");
-    run_tma<64, 64, 4, 8, 3, 2, AK, BNC>(p, "tmaT 64x64x32 4x8 st3");
-    run_tma<64, 64, 4, 8, 3, 2, AK, BNC, true>(p, "XP 64x64x32 4x8 st3");
+    run_tma<64, 64, 4, 8, 2, 2, AK, BNC>(p, "tma 64x64x32 4x8 st2");
+    run_tma<64, 32, 4, 4, 3, 2, AK, BNC>(p, "tma 64x32x32 4x4 st3");
+    run_tma<32, 64, 4, 8, 3, 2, AK, BNC>(p, "tma 32x64x32 4x8 st3 (64t)");
+    run_tma<32, 32, 4, 4, 3, 2, AK, BNC>(p, "tma 32x32x32 4x4 st3 (64t)");
+    run_tma<64, 64, 4, 4, 3, 2, AK, BNC>(p, "tma 64x64x32 4x4 st3 (256t)");
+    run_tma<128, 32, 4, 4, 3, 2, AK, BNC>(p, "tma 128x32x32 4x4 st3 (256t)");
   }
 }
 
