@@ -59,6 +59,16 @@ struct HsCfg {
 // skips the K rows >= 32.  Either way every chunk's slot and smem offset is a
 // compile-time function of j plus a per-thread constant, so the loop body is
 // a handful of integer ops and one cp.async, with no divergence.
+// inst[idx] for a lane-dependent idx without dynamic indexing (which would
+// put the 4 pointers in local memory and add a local load per chunk).
+__device__ __forceinline__ const __half* pick4(const __half* const (&inst)[4], int idx) {
+  const __half* r = inst[0];
+  r = idx == 1 ? inst[1] : r;
+  r = idx == 2 ? inst[2] : r;
+  r = idx == 3 ? inst[3] : r;
+  return r;
+}
+
 template <int ROWS, int SLOT, bool MN, bool VEC, bool K32>
 __device__ __forceinline__ void small_fill(uint8_t* smem, const __half* const (&inst)[4], const __half* any,
                                            int64_t ld, int extent, int64_t k0, int k_left, int tid) {
@@ -90,7 +100,7 @@ __device__ __forceinline__ void small_fill(uint8_t* smem, const __half* const (&
       eoff = (k0 + r) * ld + idx;
       off = off0 + sub * 8192 + (j & 3) * 2048;
     }
-    const __half* base = inst[slot];
+    const __half* base = pick4(inst, slot);
     if (base == nullptr || valid < 0) valid = 0;
     const __half* src = valid > 0 ? base + eoff : any;
     if (VEC) {
@@ -147,7 +157,7 @@ struct SmallFillPlan {
         base = inst[slot];
       } else {
         const int c = threadIdx.x & 7;
-        base = inst[((j >> 2) * 64 + c * 8) / SLOT];
+        base = pick4(inst, ((j >> 2) * 64 + c * 8) / SLOT);
       }
       uint32_t nb = bytes[j];
       if (base == nullptr) nb = 0;
