@@ -884,8 +884,7 @@ int tb_im2col(int prec, int64_t channels, int64_t height, int64_t width, int64_t
   Im2colGeom g;
   g.rows = channels * kernel_h * kernel_w;
   g.cols = out_h * out_w;
-  const int tr = prec == TB_PREC_H ? Im2colTile<uint16_t>::TR : Im2colTile<uint32_t>::TR;
-  const int64_t grid_y = (g.rows + tr - 1) / tr;
+  const int64_t grid_y = (g.rows + IM2COL_TR - 1) / IM2COL_TR;
   if (channels > lim || height > lim || width > lim || kernel_h * kernel_w > lim || height * width > lim ||
       pad_h > lim || pad_w > lim || pad_h < -lim || pad_w < -lim || stride_h > lim || stride_w > lim || dilation_h > lim || dilation_w > lim ||
       out_h > lim || out_w > lim || g.rows > lim || g.cols > lim || channels * height * width > lim ||
@@ -904,24 +903,13 @@ int tb_im2col(int prec, int64_t channels, int64_t height, int64_t width, int64_t
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const char* name;
   if (prec == TB_PREC_S) {
-    const bool al = aligned_elems(col, col_off, 4, 4);
-    if (al)
-      im2col_kernel<uint32_t, true><<<grid, block, 0, st>>>(static_cast<const uint32_t*>(im) + im_off,
-                                                              static_cast<uint32_t*>(col) + col_off, g);
-    else
-      im2col_kernel<uint32_t, false><<<grid, block, 0, st>>>(static_cast<const uint32_t*>(im) + im_off,
-                                                               static_cast<uint32_t*>(col) + col_off, g);
+    im2col_kernel<uint32_t><<<grid, block, 0, st>>>(static_cast<const uint32_t*>(im) + im_off,
+                                                      static_cast<uint32_t*>(col) + col_off, g);
     name = "im2col_b32";
   } else if (prec == TB_PREC_H) {
-    // 4-byte stores of two halves need every output column to start 4-byte aligned
-    const bool al = aligned_elems(col, col_off, 2, 4) && (g.rows % 2 == 0);
-    if (al)
-      im2col_kernel<uint16_t, true><<<grid, block, 0, st>>>(static_cast<const uint16_t*>(im) + im_off,
-                                                              static_cast<uint16_t*>(col) + col_off, g);
-    else
-      im2col_kernel<uint16_t, false><<<grid, block, 0, st>>>(static_cast<const uint16_t*>(im) + im_off,
-                                                               static_cast<uint16_t*>(col) + col_off, g);
-    name = al ? "im2col_b16x2" : "im2col_b16";
+    im2col_kernel<uint16_t><<<grid, block, 0, st>>>(static_cast<const uint16_t*>(im) + im_off,
+                                                      static_cast<uint16_t*>(col) + col_off, g);
+    name = "im2col_b16";
   } else {
     snprintf(g_last_err, sizeof(g_last_err), "im2col: precision must be H or S");
     return TB_ERR_UNSUPPORTED;
