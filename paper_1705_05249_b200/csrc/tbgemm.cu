@@ -286,6 +286,16 @@ int dispatch_sgemm_tma(const Call& c, int tile) {
     if (bmn) return launch_stma<64, 32, 4, 4, 3, false, true>(c);
     return launch_stma<64, 32, 4, 4, 3, false, false>(c);
   }
+  // 128x64 tiles that fill (nearly) whole waves of one tile per SM: 256
+  // threads of 4x8 beat two 64x64 CTAs per SM by 3-7 % (tools/sgemm_ms_bench.cu:
+  // 1024^3 56 -> 53 us, 1536^3 148 -> 143 us; both-K-contiguous layouts lose)
+  const int64_t tiles128x64 = ((p.m + 127) / 128) * ((p.n + 63) / 64) * p.batch;
+  const int64_t waves = (tiles128x64 + sms - 1) / sms;
+  if (tile == 0 && !one_tile && (amn || bmn) && waves <= 2 && tiles128x64 * 20 >= waves * sms * 17) {
+    if (amn && bmn) return launch_stma<128, 64, 4, 8, 4, true, true>(c);
+    if (amn) return launch_stma<128, 64, 4, 8, 4, true, false>(c);
+    return launch_stma<128, 64, 4, 8, 4, false, true>(c);
+  }
   if (amn && bmn) return launch_stma<64, 64, 4, 8, 3, true, true>(c);
   if (amn) return launch_stma<64, 64, 4, 8, 3, true, false>(c);
   if (bmn) return launch_stma<64, 64, 8, 4, 4, false, true>(c);

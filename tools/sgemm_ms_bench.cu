@@ -112,6 +112,32 @@ void suite(Problem p) {
     run_tma<32, 32, 4, 4, 3, 2, AK, BNC>(p, "tma 32x32x32 4x4 st3 (64t)");
     run_tma<64, 64, 4, 4, 3, 2, AK, BNC>(p, "tma 64x64x32 4x4 st3 (256t)");
     run_tma<128, 32, 4, 4, 3, 2, AK, BNC>(p, "tma 128x32x32 4x4 st3 (256t)");
+    // <= 148 tiles at 1024^2: one CTA per SM, larger micro-tiles
+    run_tma<128, 64, 8, 8, 3, 1, AK, BNC>(p, "tma 128x64x32 8x8 st3 (128t)");
+    run_tma<128, 64, 8, 8, 4, 1, AK, BNC>(p, "tma 128x64x32 8x8 st4 (128t)");
+    run_tma<128, 64, 8, 4, 4, 1, AK, BNC>(p, "tma 128x64x32 8x4 st4 (256t)");
+    run_tma<128, 64, 4, 8, 4, 1, AK, BNC>(p, "tma 128x64x32 4x8 st4 (256t)");
+    run_tma<64, 128, 8, 8, 4, 1, AK, BNC>(p, "tma 64x128x32 8x8 st4 (128t)");
+    run_tma<64, 128, 4, 8, 4, 1, AK, BNC>(p, "tma 64x128x32 4x8 st4 (256t)");
+    run_tma<64, 64, 4, 4, 4, 2, AK, BNC>(p, "tma 64x64x32 4x4 st4 (256t)");
+    run_tma<64, 64, 8, 4, 4, 2, AK, BNC>(p, "tma 64x64x32 8x4 st4");
+    run_tma<64, 64, 4, 8, 4, 2, AK, BNC>(p, "tma 64x64x32 4x8 st4");
+  } else if constexpr (AK && BNC) {
+    // library: 64x64 8x4 st4 (PAIR_N)
+    run_tma<64, 64, 8, 4, 4, 2, AK, BNC>(p, "tma 64x64x32 8x4 st4");
+    run_tma<128, 64, 8, 4, 4, 1, AK, BNC>(p, "tma 128x64x32 8x4 st4 (256t)");
+    run_tma<128, 64, 4, 8, 4, 1, AK, BNC>(p, "tma 128x64x32 4x8 st4 (256t)");
+    run_tma<64, 128, 4, 8, 4, 1, AK, BNC>(p, "tma 64x128x32 4x8 st4 (256t)");
+  } else if constexpr (!AK && BNC) {
+    // library: 64x64 4x8 st3
+    run_tma<64, 64, 4, 8, 3, 2, AK, BNC>(p, "tma 64x64x32 4x8 st3");
+    run_tma<128, 64, 4, 8, 4, 1, AK, BNC>(p, "tma 128x64x32 4x8 st4 (256t)");
+    run_tma<64, 128, 4, 8, 4, 1, AK, BNC>(p, "tma 64x128x32 4x8 st4 (256t)");
+  } else {
+    // library: 64x64 4x8 st3 (A transposed in shared memory)
+    run_tma<64, 64, 4, 8, 3, 2, AK, BNC>(p, "tma 64x64x32 4x8 st3");
+    run_tma<128, 64, 4, 8, 4, 1, AK, BNC>(p, "tma 128x64x32 4x8 st4 (256t)");
+    run_tma<64, 128, 4, 8, 4, 1, AK, BNC>(p, "tma 64x128x32 4x8 st4 (256t)");
   }
 }
 
