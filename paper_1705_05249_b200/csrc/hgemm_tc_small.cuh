@@ -39,6 +39,8 @@ struct HsCfg {
   static constexpr int STAGES = (196608 / STAGE_BYTES) > 8 ? 8 : (196608 / STAGE_BYTES);  // <= 192 KB ring
   static constexpr int DEPTH = STAGES - 1;
   static constexpr int ACC = (BN <= 128) ? 4 : 2;
+  // k <= 32: pair two tiles per stage (doubles the bytes in flight per ring slot)
+  static constexpr bool PAIR = true;
   static constexpr int TMEM_COLS = (ACC * BN <= 256) ? 256 : 512;
   // warps 0-7 epilogue (TMEM quadrant w%4, column half w/4), 8-11 producer,
   // 12 TMEM allocation + MMA issue
@@ -144,7 +146,12 @@ struct SmallFillPlan {
       bytes[j] = valid > 0 ? static_cast<uint32_t>(valid) * 2u : 0u;
     }
   }
+  // HI (K32 only): place the chunks in K columns 32..63 of the stage instead
+  // (the second tile of a paired stage): chunk c -> c ^ 4 inside the 128-byte
+  // K-major row, or the next two 8-row K atoms of an MN-major sub-tile.
+  template <bool HI = false>
   __device__ __forceinline__ void issue(uint8_t* smem, const __half* const (&inst)[4], const __half* any) const {
+    static_assert(!HI || K32, "hi half is only free when k <= 32");
 #pragma unroll
     for (int j = 0; j < PER_T; ++j) {
       if (K32 && MN && (j & 3) >= 2) continue;  // K rows 32..63: never read
@@ -161,7 +168,8 @@ struct SmallFillPlan {
       }
       uint32_t nb = bytes[j];
       if (base == nullptr) nb = 0;
-      cp_async_16(smem + off[j], nb ? base + eoff[j] : any, nb);
+      const uint32_t o = HI ? (MN ? off[j] + 4096u : (off[j] ^ 64u)) : off[j];
+      cp_async_16(smem + o, nb ? base + eoff[j] : any, nb);
     }
   }
 };
@@ -191,7 +199,7 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
     }
     for (int a = 0; a < ACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 32 * C::EPI_WARPS);
+      mbar_init(&tempty[a], 32 * 4);  // one warp group per tile
     }
     fence_mbar_init();
   }
@@ -220,10 +228,25 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
       plan_a.init(p.lda, m, k_left, tid);
       plan_b.init(p.ldb, n, k_left, tid);
     }
-    for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    // K32: two tiles per stage (t in K columns 0..31, t + gridDim.x in 32..63)
+    constexpr bool PAIR = C::PAIR && K32 && VEC;
+    const int64_t tstep = PAIR ? 2 * static_cast<int64_t>(gridDim.x) : gridDim.x;
+    for (int64_t t = blockIdx.x; t < total_tiles; t += tstep) {
       const int64_t zbase = t * P;
       const __half* ia[4];
       const __half* ib[4];
+      const __half* ja[4];
+      const __half* jb[4];
+      if constexpr (PAIR) {
+        const int64_t z1 = (t + gridDim.x) * P;
+#pragma unroll
+        for (int sl = 0; sl < 4; ++sl) {
+          const int64_t zi = z1 + sl;
+          const bool ok = sl < P && zi < p.batch;
+          ja[sl] = ok ? A + inst_off(p.a_off, p.stride_a, p.a_offs, zi) : nullptr;
+          jb[sl] = ok ? B + inst_off(p.b_off, p.stride_b, p.b_offs, zi) : nullptr;
+        }
+      }
 #pragma unroll
       for (int sl = 0; sl < 4; ++sl) {
         const int64_t zi = zbase + sl;
@@ -235,7 +258,12 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
         mbar_wait(&empty[s], ph ^ 1);
         const int64_t k0 = static_cast<int64_t>(kb) * HG_BK;
         const int k_left = static_cast<int>(min64(HG_BK, p.k - k0));
-        if (one_block) {
+        if constexpr (PAIR) {
+          plan_a.issue(sA + s * C::A_BYTES, ia, A);
+          plan_b.issue(sB + s * C::B_BYTES, ib, B);
+          plan_a.template issue<true>(sA + s * C::A_BYTES, ja, A);
+          plan_b.template issue<true>(sB + s * C::B_BYTES, jb, B);
+        } else if (one_block) {
           plan_a.issue(sA + s * C::A_BYTES, ia, A);
           plan_b.issue(sB + s * C::B_BYTES, ib, B);
         } else {
@@ -273,6 +301,34 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
     constexpr uint32_t idesc = umma_idesc_f16(128, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
     int s = 0, acc = 0;
     uint32_t ph = 0, aph = 0;
+    if constexpr (C::PAIR && K32 && VEC) {
+      // one stage = two tiles; the second one's K16 steps start 2 steps in
+      // (the descriptors of steps 2, 3 of a full block: same MMA sequence)
+      const int ksteps = hg_ksteps(p.k, 0);
+      constexpr uint32_t A_HI = A_MN ? 4096u : 64u, B_HI = B_MN ? 4096u : 64u;
+      for (int64_t t = blockIdx.x; t < total_tiles; t += 2 * static_cast<int64_t>(gridDim.x)) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(sA + s * C::A_BYTES);
+        const uint32_t b_addr = smem_u32(sB + s * C::B_BYTES);
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          if (t + h * static_cast<int64_t>(gridDim.x) >= total_tiles) break;
+          mbar_wait(&tempty[acc], aph ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+          if (elect_one()) {
+            hg_issue_kblock<A_MN, B_MN>(Mma1Sm{}, d_tmem, a_addr + h * A_HI, b_addr + h * B_HI, idesc, ksteps, true);
+            tc_commit(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++acc == ACC) { acc = 0; aph ^= 1; }
+        }
+        if (elect_one()) tc_commit(&empty[s]);
+        __syncwarp();
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+    } else
     for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
       mbar_wait(&tempty[acc], aph ^ 1);
       tc_fence_after();
@@ -296,12 +352,18 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
     }
   } else if (warp < C::EPI_WARPS) {
     // ===================== epilogue =====================
+    // Warp group g = warp / 4 takes every other tile (tile sequence index
+    // i = 2j + g of this CTA), each warp the full NI columns of its TMEM lane
+    // quadrant: two tiles drain concurrently (one tile at a time was the
+    // per-tile latency floor of the batched small path).
     const int quad = warp & 3;
-    const int half = warp >> 2;
+    const int grp = warp >> 2;
     const int slot = (quad * 32) / MI;
-    int acc = 0;
-    uint32_t aph = 0;
-    for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    int64_t seq = grp;
+    for (int64_t t = blockIdx.x + static_cast<int64_t>(grp) * gridDim.x; t < total_tiles;
+         t += 2 * static_cast<int64_t>(gridDim.x), seq += 2) {
+      const int acc = static_cast<int>(seq % ACC);
+      const uint32_t aph = static_cast<uint32_t>((seq / ACC) & 1);
       const int64_t zi = t * P + slot;
       const bool inst_ok = zi < p.batch;
       Epi epi;
@@ -316,26 +378,17 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                              static_cast<uint32_t>(acc * BN + slot * NI);
-      // NI = 64: each column half takes one 32-column chunk; NI = 32: each
-      // half takes 16 columns (x16 TMEM loads).
-      if (NI == 64) {
+#pragma unroll
+      for (int h = 0; h < NI / 32; ++h) {
         uint32_t v[32];
-        tmem_ld_32x32b_x32(t_row + half * 32, v);
+        tmem_ld_32x32b_x32(t_row + h * 32, v);
         tmem_ld_wait();
-        if (rows_valid > 0 && half * 32 < n)
-          epi_store_block<32>(stage, v, Cz + static_cast<int64_t>(half * 32) * p.ldc + row0, p.ldc, rows_valid,
-                              n - half * 32, epi, lane);
-      } else {
-        uint32_t v[16];
-        tmem_ld_32x32b_x16(t_row + half * 16, v);
-        tmem_ld_wait();
-        if (rows_valid > 0 && half * 16 < n)
-          epi_store_block<16>(stage, v, Cz + static_cast<int64_t>(half * 16) * p.ldc + row0, p.ldc, rows_valid,
-                              n - half * 16, epi, lane);
+        if (rows_valid > 0 && h * 32 < n)
+          epi_store_block<32>(stage, v, Cz + static_cast<int64_t>(h * 32) * p.ldc + row0, p.ldc, rows_valid,
+                              n - h * 32, epi, lane);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      if (++acc == ACC) { acc = 0; aph ^= 1; }
     }
   }
   tc_fence_before();
