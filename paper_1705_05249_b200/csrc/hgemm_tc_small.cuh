@@ -42,7 +42,7 @@ struct HsCfg {
   // k <= 32: pair two tiles per stage (doubles the bytes in flight per ring slot)
   static constexpr bool PAIR = true;
   static constexpr int TMEM_COLS = (ACC * BN <= 256) ? 256 : 512;
-  // warps 0-7 epilogue (TMEM quadrant w%4, column half w/4), 8-11 producer,
+  // warps 0-7 epilogue (TMEM quadrant w%4, warp group w/4 takes alternate tiles), 8-11 producer,
   // 12 TMEM allocation + MMA issue
   static constexpr int EPI_WARPS = 8, PROD_WARP0 = 8, MMA_WARP = 12;
   static constexpr int THREADS = 13 * 32;
