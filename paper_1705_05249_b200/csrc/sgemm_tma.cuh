@@ -51,12 +51,17 @@ struct TmaSgemmCfg {
   static constexpr bool B_T = !B_MN && XP;
   static constexpr bool PAIR_N = !A_MN && !A_T;
   static constexpr int A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  // B slot rounded up to 1024 bytes (BN = 60: 7680 B of data in an 8 KB slot)
+  static constexpr int B_ALLOC = (B_BYTES + 1023) / 1024 * 1024;
+  static constexpr int STAGE_BYTES = A_BYTES + B_ALLOC;
+  static constexpr int TX_BYTES = A_BYTES + B_BYTES;  // bytes the two TMA boxes land
   static constexpr int T_BYTES = (A_T ? 2 * A_BYTES : 0) + (B_T ? 2 * B_BYTES : 0);
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + T_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(BK == 32, "K-contiguous tiles are 128-byte SWIZZLE_128B rows");
   static_assert(TM % 4 == 0 && TN % 4 == 0 && NT % 32 == 0, "tile shape");
-  static_assert(A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0, "1024-byte aligned stage tiles");
+  static_assert(A_BYTES % 1024 == 0, "1024-byte aligned stage tiles");
+  static_assert(!A_T || (BM * (BK / 4)) % NT == 0, "A transpose covers the tile");
+  static_assert(!B_T || (BN * (BK / 4)) % NT == 0, "B transpose covers the tile");
 };
 
 template <int TM, int TN>
@@ -121,7 +126,7 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
     const int s = t % STAGES;
     uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
     uint8_t* sb = sa + Cfg::A_BYTES;
-    mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+    mbar_arrive_expect_tx(&full[s], Cfg::TX_BYTES);
     if (A_MN) tma_load_3d(sa, &tmap_a, &full[s], m0, t * BK, z);
     else      tma_load_3d(sa, &tmap_a, &full[s], t * BK, m0, z);
     if (B_MN) tma_load_3d(sb, &tmap_b, &full[s], n0, t * BK, z);
