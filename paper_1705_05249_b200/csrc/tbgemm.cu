@@ -211,7 +211,7 @@ int launch_simt(const Call& c, const char* tag) {
 
 // TMA-fed FFMA2 SGEMM (sgemm_tma.cuh).  M/N-contiguous operands: box
 // {ROWS, 32} without swizzle; K-contiguous: box {32, ROWS} SWIZZLE_128B.
-template <int BM, int BN, int TM, int TN, int ST, bool AMN, bool BMN, bool XP = false>
+template <int BM, int BN, int TM, int TN, int ST, bool AMN, bool BMN, bool XP = false, int MINB = 2>
 int launch_stma(const Call& c) {
   using Cfg = TmaSgemmCfg<BM, BN, 32, TM, TN, ST, AMN, BMN, XP>;
   const Problem& p = c.p;
@@ -231,7 +231,7 @@ int launch_stma(const Call& c) {
   const int tiles_n = static_cast<int>((p.n + BN - 1) / BN);
   const int64_t blocks = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
   if (blocks > 0x7fffffffLL) return TB_ERR_INVALID;
-  auto kern = sgemm_tma_kernel<BM, BN, 32, TM, TN, ST, AMN, BMN, 2, XP>;
+  auto kern = sgemm_tma_kernel<BM, BN, 32, TM, TN, ST, AMN, BMN, MINB, XP>;
   static SmemAttr attr;  // per instantiation, per device
   if (int rc2 = ensure_smem(attr, kern, Cfg::SMEM_BYTES)) return rc2;
   dim3 grid(static_cast<unsigned>(blocks)), block(Cfg::NT);
@@ -261,6 +261,14 @@ int dispatch_sgemm_tma(const Call& c, int tile) {
   // keep every SM busy (1024^3 37.6, C3 (4096,128,9216) 34.8 TFLOP/s).
   if (tile == 3) {
     // batched instances of at most 32x32: one 32x32 tile each, 64 threads of 4x4
+    // k <= 32 is a single K block: one ring slot and a 64-register cap, so 16
+    // CTAs per SM fit (2 slots at 92 registers: 10)
+    if (p.k <= 32) {
+      if (amn && bmn) return launch_stma<32, 32, 4, 4, 1, true, true, false, 16>(c);
+      if (amn) return launch_stma<32, 32, 4, 4, 1, true, false, false, 16>(c);
+      if (bmn) return launch_stma<32, 32, 4, 4, 1, false, true, true, 16>(c);
+      return launch_stma<32, 32, 4, 4, 1, false, false, true, 16>(c);
+    }
     if (amn && bmn) return launch_stma<32, 32, 4, 4, 2, true, true>(c);
     if (amn) return launch_stma<32, 32, 4, 4, 2, true, false>(c);
     if (bmn) return launch_stma<32, 32, 4, 4, 2, false, true, true>(c);
