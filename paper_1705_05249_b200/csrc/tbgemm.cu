@@ -304,6 +304,14 @@ int dispatch_sgemm_tma(const Call& c, int tile) {
     if (amn) return launch_stma<128, 64, 4, 8, 4, true, false>(c);
     return launch_stma<128, 64, 4, 8, 4, false, true>(c);
   }
+  // batched instances of at most 64x64 with k <= 64 (two K blocks): a
+  // two-slot ring and a 102-register cap, 5 CTAs per SM instead of 4
+  if (one_tile && p.k <= 64) {
+    if (amn && bmn) return launch_stma<64, 64, 4, 8, 2, true, true, false, 5>(c);
+    if (amn) return launch_stma<64, 64, 4, 8, 2, true, false, false, 5>(c);
+    if (bmn) return launch_stma<64, 64, 8, 4, 2, false, true, false, 5>(c);
+    return launch_stma<64, 64, 4, 8, 2, false, false, false, 5>(c);
+  }
   if (amn && bmn) return launch_stma<64, 64, 4, 8, 3, true, true>(c);
   if (amn) return launch_stma<64, 64, 4, 8, 3, true, false>(c);
   if (bmn) return launch_stma<64, 64, 8, 4, 4, false, true>(c);
