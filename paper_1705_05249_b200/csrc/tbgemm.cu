@@ -262,7 +262,8 @@ int dispatch_sgemm_tma(const Call& c, int tile) {
   if (tile == 3) {
     // batched instances of at most 32x32: one 32x32 tile each, 64 threads of 4x4
     // k <= 32 is a single K block: one ring slot and a 51-register cap, so 20
-    // CTAs per SM fit (2 slots at 92 registers: 10; 49.0 -> 44.3 us at S32)
+    // CTAs per SM fit (2 slots at 92 registers: 10; 49.0 -> 44.3 us at S32;
+    // a 42-register cap, 24 CTAs, spills: 47.0 us)
     if (p.k <= 32) {
       if (amn && bmn) return launch_stma<32, 32, 4, 4, 1, true, true, false, 20>(c);
       if (amn) return launch_stma<32, 32, 4, 4, 1, true, false, false, 20>(c);
