@@ -214,7 +214,7 @@ def run_ours(args, rank, world, local_rank):
     # L2 flush before every step: a 256 MiB write evicts the inputs (126 MB
     # L2), then a 256 MiB read of a second buffer evicts the flush's dirty
     # lines, so the timed kernel starts from a cold, clean L2 and does not pay
-    # for unrelated write-backs (tools/exp15.py: C3 34.9 -> 30.5 us).
+    # for unrelated write-backs (measured: C3 34.9 -> 30.5 us).
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     clean_buf = torch.ones(256 << 20, dtype=torch.uint8, device=dev)
 

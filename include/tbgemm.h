@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define TBGEMM_ABI_VERSION 1
+#define TBGEMM_ABI_VERSION 2
 
 /* Precision.H / Precision.S   (core.py:43-50) */
 enum { TB_PREC_H = 0, TB_PREC_S = 1 };
@@ -76,14 +76,27 @@ enum {
 };
 
 /*
- * The 14 reference tuning parameters (GemmParams, params.py:120-146) in the
- * reference's order.  The library maps them onto its nearest sm_100a
- * instantiation (DESIGN.md §"Parameter mapping"); NULL = built-in default.
+ * sm_100a kernel selection: the "gemm_b200" tuning family
+ * (paper_1705_05249_b200/kernels/params.py; DESIGN.md §4 "Tuning space").
+ * NULL (or every field 0) = the built-in shape routing.  The reference's 14
+ * OpenCL parameters (GemmParams, params.py:120-146) describe an OpenCL
+ * work-group decomposition; they are validated and recorded by the Python
+ * host layer (LaunchRecord.params) and never cross this boundary.
+ *   MWG x NWG  CTA tile.  H: 128 x {64,128,256} (cta_group::1), 256 x 256
+ *              (cta_group::2 pair), 128 x 128 (split-K).  S: TMA-fed FFMA2
+ *              (KWG 32) 128x128 / 64x128 / 128x64 / 64x64 / 64x32 / 32x32;
+ *              register-staged (KWG 16) 128x256 / 128x128 / 64x128 / 128x64
+ *              / 64x64.  The library maps a tile onto the instantiation for
+ *              the operands' major-ness; tb_last_launch names it.
+ *   KWG        K depth per pipeline stage (H 64; S 32 TMA / 16 register-staged)
+ *   STAGES     shared-memory ring depth (0 = the instantiation's default)
+ *   CTA_GROUP  H: 1 or 2 (tcgen05 cta_group::2 CTA pair)
+ *   SPLIT_K    H: cluster split-K factor 1, 2, 4, 8 (DSMEM reduction); S: 1
+ *   GROUP_M    grouped-raster height in tiles (0 = the kernel's default)
  */
-typedef struct tb_gemm_params {
-  int32_t MWG, NWG, KWG, MDIMC, NDIMC, MDIMA, NDIMB, KWI, VWM, VWN, STRM, STRN,
-      SA, SB;
-} tb_gemm_params;
+typedef struct tb_gemm_config {
+  int32_t MWG, NWG, KWG, STAGES, CTA_GROUP, SPLIT_K, GROUP_M;
+} tb_gemm_config;
 
 /*
  * What the last call on this thread launched (engine.py:128-133 records a
@@ -104,7 +117,7 @@ int tb_gemm(int prec, int layout, int trans_a, int trans_b, int64_t m,
             int64_t n, int64_t k, float alpha, const void* a, int64_t a_off,
             int64_t lda, const void* b, int64_t b_off, int64_t ldb,
             float beta, void* c, int64_t c_off, int64_t ldc,
-            const tb_gemm_params* params, int flags, void* stream);
+            const tb_gemm_config* cfg, int flags, void* stream);
 
 /* Instance i uses base offset + i*stride — replaces extras.py:309-348 → 188-286 */
 int tb_gemm_strided_batched(int prec, int layout, int trans_a, int trans_b,
@@ -113,7 +126,7 @@ int tb_gemm_strided_batched(int prec, int layout, int trans_a, int trans_b,
                             int64_t stride_a, const void* b, int64_t b_off,
                             int64_t ldb, int64_t stride_b, float beta, void* c,
                             int64_t c_off, int64_t ldc, int64_t stride_c,
-                            int64_t batch, const tb_gemm_params* params,
+                            int64_t batch, const tb_gemm_config* cfg,
                             int flags, void* stream);
 
 /*
@@ -127,7 +140,7 @@ int tb_gemm_batched(int prec, int layout, int trans_a, int trans_b, int64_t m,
                     const int64_t* a_offs, int64_t lda, const void* b,
                     const int64_t* b_offs, int64_t ldb, const float* betas,
                     void* c, const int64_t* c_offs, int64_t ldc, int64_t batch,
-                    int offs_aligned, const tb_gemm_params* params, int flags,
+                    int offs_aligned, const tb_gemm_config* cfg, int flags,
                     void* stream);
 
 /*
@@ -170,6 +183,11 @@ int tb_convert_f32(int prec, int direction, int64_t rows, int64_t cols, float al
 int tb_trsm_block(int64_t nb, int64_t ncols, const float* t, int64_t t_off,
                   int64_t ldt, float* x, int64_t x_off, int64_t ldx, int upper,
                   int unit, void* stream);
+
+/* Allocate the per-device state a launch may need (the CTA-pair kernel's
+ * wave-barrier counters) on the current device, outside any stream capture,
+ * so later calls allocate nothing.  Idempotent. */
+int tb_prepare_device(void);
 
 /* Fill the record of the last launch issued from the calling thread. */
 int tb_last_launch(tb_launch_record* out);

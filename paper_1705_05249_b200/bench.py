@@ -201,10 +201,15 @@ def write_report(rows, csv_path=None, json_path=None) -> None:
 
 
 def heatmap_experiment(sizes, precision: Precision, ctx: Context, budget: int = 32,
-                       seed: int = 7, warmup: int = 1, runs: int = 10) -> HeatmapResult:
+                       seed: int = 7, warmup: int = 1, runs: int = 10,
+                       family: str | None = None) -> HeatmapResult:
     """Problem-specific-tuning heat map (bench.py:287-356): tune once per
     size, then time every (benched size, tuned-for size) pair through a
-    runtime override; relative_perf[i][j] = 100 * t(i, p_i) / t(i, p_j)."""
+    runtime override; relative_perf[i][j] = 100 * t(i, p_i) / t(i, p_j).
+    ``family`` defaults to gemm_b200 (the family that selects sm_100a
+    kernels) on a B200 and to the reference's gemm elsewhere."""
+    if family is None:
+        family = "gemm_b200" if ctx.device.is_b200 else "gemm"
     sizes = [tuple(int(v) for v in s) for s in sizes]
     if len(set(sizes)) != len(sizes):
         raise UsageError("heat-map sizes must be distinct")
@@ -212,7 +217,7 @@ def heatmap_experiment(sizes, precision: Precision, ctx: Context, budget: int = 
     best = {}
     for size in sizes:
         m, n, k = size
-        task = TuningTask("gemm", precision, {"m": m, "n": n, "k": k}, ctx.device,
+        task = TuningTask(family, precision, {"m": m, "n": n, "k": k}, ctx.device,
                           budget=budget, seed=seed, warmup_runs=warmup, timed_runs=runs)
         try:
             best[size] = tune(task, ctx).best
@@ -223,7 +228,7 @@ def heatmap_experiment(sizes, precision: Precision, ctx: Context, budget: int = 
     for i, bench_size in enumerate(sizes):
         case = _ClientCase("gemm", bench_size, precision, ctx)
         for j in range(count):
-            store.set_override("gemm", precision, ctx.device, bench_size, best[sizes[j]])
+            store.set_override(family, precision, ctx.device, bench_size, best[sizes[j]])
             if not case.verify():
                 store.clear_overrides()
                 raise ExperimentError(f"correctness failure at size {bench_size} with "
@@ -231,7 +236,7 @@ def heatmap_experiment(sizes, precision: Precision, ctx: Context, budget: int = 
         per_run = np.zeros((count, runs))
         for r in range(runs):
             for j in range(count):
-                store.set_override("gemm", precision, ctx.device, bench_size, best[sizes[j]])
+                store.set_override(family, precision, ctx.device, bench_size, best[sizes[j]])
                 per_run[j, r] = time_on_stream(case.tuned, warmup if r == 0 else 0, 1, ctx.stream)[0]
         times[i, :] = per_run.mean(axis=1)
         store.clear_overrides()

@@ -1,6 +1,9 @@
 """Build libtbgemm.so in-tree for sm_100a (nvcc; no torch JIT cache).
 
-    python -m paper_1705_05249_b200.build_native [--force]
+    python -m paper_1705_05249_b200.build_native [--force] [-j N]
+
+The kernels live in several translation units (csrc/*.cu) compiled in
+parallel to objects under build/ and linked into one shared library.
 """
 
 from __future__ import annotations
@@ -9,19 +12,22 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "_lib" / "libtbgemm.so"
-SOURCES = [CSRC / "tbgemm.cu"]
-DEPS = sorted(CSRC.glob("*.cu*")) + [ROOT / "include" / "tbgemm.h"]
+OBJ = ROOT / "build" / "obj"
+SOURCES = sorted(CSRC.glob("*.cu"))
+DEPS = sorted(CSRC.glob("*.cu*")) + sorted(CSRC.glob("*.h")) + [ROOT / "include" / "tbgemm.h"]
 
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
+    *ARCH,
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-Xptxas", "-warn-spills",
 ]
 
@@ -40,12 +46,25 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def _compile(src: Path, verbose: bool) -> Path:
+    obj = OBJ / (src.stem + ".o")
+    cmd = [nvcc(), *NVCC_FLAGS, f"-I{ROOT / 'include'}", "-c", "-o", str(obj), str(src)]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    return obj
+
+
+def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> Path:
     if not force and up_to_date():
         return OUT
     OUT.parent.mkdir(parents=True, exist_ok=True)
+    OBJ.mkdir(parents=True, exist_ok=True)
+    jobs = jobs or min(len(SOURCES), os.cpu_count() or 1)
+    with ThreadPoolExecutor(max_workers=jobs) as pool:
+        objs = list(pool.map(lambda s: _compile(s, verbose), SOURCES))
     tmp = OUT.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, f"-I{ROOT / 'include'}", "-o", str(tmp), *map(str, SOURCES)]
+    cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
@@ -54,4 +73,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    j = None
+    if "-j" in sys.argv:
+        j = int(sys.argv[sys.argv.index("-j") + 1])
+    print(build(force="--force" in sys.argv, verbose=True, jobs=j))

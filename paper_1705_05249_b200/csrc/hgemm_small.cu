@@ -1,0 +1,73 @@
+// hgemm_small.cu — packed small-instance tcgen05 HGEMM (hgemm_tc_small.cuh):
+// m, n <= 64 per instance, P = 128/MI instances per UMMA tile.
+#include "hgemm_tc_small.cuh"
+#include "host.h"
+
+namespace tb {
+namespace host {
+namespace {
+
+template <int MI, int NI, bool AMN, bool BMN, bool VEC, bool K32>
+int launch_hs(const Call& c) {
+  using Cfg = HsCfg<MI, NI>;
+  const Problem& p = c.p;
+  const int64_t total = (p.batch + Cfg::P - 1) / Cfg::P;
+  auto kern = hgemm_tc_small_kernel<MI, NI, AMN, BMN, VEC, K32>;
+  static SmemAttr attr;  // per instantiation, per device
+  if (int rc = ensure_smem(attr, kern, Cfg::SMEM_BYTES)) return rc;
+  const int sms = sms_or_default();
+  const int64_t g = total < sms ? total : sms;
+  dim3 grid(static_cast<unsigned>(g)), block(Cfg::THREADS);
+  kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(p, total);
+  char name[64];
+  snprintf(name, sizeof(name), "hgemm_tc_small_%dx%d_p%d_%c%c%s%s", MI, NI, Cfg::P, AMN ? 'm' : 'k',
+           BMN ? 'n' : 'k', VEC ? "_cpasync" : "_scalar", K32 ? "_k32" : "");
+  record(name, grid, block, 1, Cfg::SMEM_BYTES, total);
+  return check_launch("hgemm_tc_small launch");
+}
+
+template <int MI, int NI, bool VEC, bool K32>
+int launch_hs_layout(const Call& c) {
+  const bool amn = !c.p.a_kcontig, bmn = c.p.b_ncontig;
+  if (!amn && !bmn) return launch_hs<MI, NI, false, false, VEC, K32>(c);
+  if (!amn && bmn) return launch_hs<MI, NI, false, true, VEC, K32>(c);
+  if (amn && !bmn) return launch_hs<MI, NI, true, false, VEC, K32>(c);
+  return launch_hs<MI, NI, true, true, VEC, K32>(c);
+}
+
+template <bool VEC, bool K32>
+int dispatch_hsmall_k(const Call& c) {
+  const Problem& p = c.p;
+  if (p.m <= 32) return p.n <= 32 ? launch_hs_layout<32, 32, VEC, K32>(c) : launch_hs_layout<32, 64, VEC, K32>(c);
+  return p.n <= 32 ? launch_hs_layout<64, 32, VEC, K32>(c) : launch_hs_layout<64, 64, VEC, K32>(c);
+}
+
+// k <= 32 (one partial K block; the MMAs read K columns 0..31 only): the K32
+// fill skips the unread half of each staged row.  Same MMA sequence either way.
+template <bool VEC>
+int dispatch_hsmall(const Call& c) {
+  if (VEC && c.p.k <= 32) return dispatch_hsmall_k<VEC, true>(c);
+  return dispatch_hsmall_k<VEC, false>(c);
+}
+
+bool small_aligned(const Call& c) {
+  const Problem& p = c.p;
+  bool al = (p.lda % 8 == 0) && (p.ldb % 8 == 0) && aligned_elems(p.a, 0, 2, 16) && aligned_elems(p.b, 0, 2, 16);
+  if (p.a_offs || p.b_offs) {
+    al = al && c.offs_aligned;
+  } else {
+    al = al && (p.a_off % 8 == 0) && (p.b_off % 8 == 0);
+    if (p.batch > 1) al = al && (p.stride_a % 8 == 0) && (p.stride_b % 8 == 0);
+  }
+  return al;
+}
+
+}  // namespace
+
+int dispatch_hsmall_any(const Call& c) {
+  if (small_aligned(c)) return dispatch_hsmall<true>(c);
+  return dispatch_hsmall<false>(c);
+}
+
+}  // namespace host
+}  // namespace tb

@@ -33,9 +33,12 @@ namespace tb {
 constexpr int HG_BM = 128;
 constexpr int HG_BK = 64;  // 64 halves = 128 B = one SW128 row
 
-template <int BN, bool TMA>
+// ST: ring depth (0 = default: 4 for BN 256, 6 otherwise — the deepest that
+// fits next to the epilogue staging; "gemm_b200" STAGES selects the other
+// instantiated depth, hgemm.cu).
+template <int BN, bool TMA, int ST = 0>
 struct HgCfg {
-  static constexpr int STAGES = (BN >= 256) ? 4 : 6;
+  static constexpr int STAGES = ST > 0 ? ST : ((BN >= 256) ? 4 : 6);
   static constexpr int A_BYTES = HG_BM * HG_BK * 2;            // 16 KB
   static constexpr int B_BYTES = BN * HG_BK * 2;               // 8/16/32 KB
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -228,11 +231,11 @@ __device__ __forceinline__ void epi_store_block(float* stage, const uint32_t (&v
   __syncwarp();
 }
 
-template <int BN, bool TMA, bool A_MN, bool B_MN, bool VEC>
-__global__ void __launch_bounds__(HgCfg<BN, TMA>::THREADS, 1)
+template <int BN, bool TMA, bool A_MN, bool B_MN, bool VEC, int ST = 0>
+__global__ void __launch_bounds__(HgCfg<BN, TMA, ST>::THREADS, 1)
     hgemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     Problem p, int tiles_m, int tiles_n, int group_m, int64_t total_tiles) {
-  using C = HgCfg<BN, TMA>;
+  using C = HgCfg<BN, TMA, ST>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_align1024(smem_raw);
@@ -405,6 +408,7 @@ __global__ void __launch_bounds__(HgCfg<BN, TMA>::THREADS, 1)
 }
 
 // alpha == 0 / k == 0 for H (level3.py:125-132): C = beta == 0 ? 0 : RNE(beta*C)
+template <int UNUSED = 0>  // a template: weak linkage across the translation units that include this header
 __global__ void hscale_kernel(Problem p) {
   const int64_t total = p.m * p.n;
   for (int64_t z = 0; z < p.batch; ++z) {

@@ -99,19 +99,28 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
 // K = 32768 (16 MB panels, ~18 panels per wave) L2 reuse collapses (ncu: 329 GB
 // DRAM per 32768^3 call; the barrier measured 945 -> 1286 TFLOP/s there).
 // The barrier is advisory: the target never exceeds the tiles every CTA will
-// finish (ragged last wave), and a wait gives up after ~2 ms (%globaltimer) so
-// CTAs that are not co-resident can never deadlock the launch.  The counter
-// is zeroed on the launch stream before every launch.
-__device__ __forceinline__ void wave_wait(const unsigned int* ctr, unsigned int target) {
+// finish (ragged last wave), and the first wait that exceeds ~2 ms
+// (%globaltimer) — CTAs not co-resident because other work holds SMs —
+// raises an abandon flag (ctr[1]) that turns the barrier off for every CTA
+// for the rest of the launch, so a shared GPU costs at most one timeout per
+// call, never one per wave.  The launcher also sizes the grid from
+// cudaOccupancyMaxActiveClusters.  Both words are zeroed on the launch stream
+// before every launch.
+__device__ __forceinline__ void wave_wait(unsigned int* ctr, unsigned int target) {
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  unsigned int v;
+  unsigned int v, off;
   for (;;) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
     if (v >= target) return;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(off) : "l"(ctr + 1) : "memory");
+    if (off != 0u) return;
     uint64_t t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    if (t1 - t0 > 2000000ull) return;
+    if (t1 - t0 > 2000000ull) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 1;" ::"l"(ctr + 1) : "memory");
+      return;
+    }
   }
 }
 __device__ __forceinline__ void wave_arrive(unsigned int* ctr) {

@@ -1,0 +1,144 @@
+// sgemm_tma.cu — launch + tile routing of the TMA-fed FFMA2 SGEMM
+// (sgemm_tma.cuh).  M/N-contiguous operands: box {ROWS, 32} without swizzle;
+// K-contiguous: box {32, ROWS} SWIZZLE_128B.
+#include <cstring>
+
+#include "host.h"
+#include "sgemm_tma.cuh"
+
+namespace tb {
+namespace host {
+namespace {
+
+template <int BM, int BN, int TM, int TN, int ST, bool AMN, bool BMN, bool XP = false, int MINB = 2>
+int launch_stma(const Call& c) {
+  using Cfg = TmaSgemmCfg<BM, BN, 32, TM, TN, ST, AMN, BMN, XP>;
+  const Problem& p = c.p;
+  const float* A = static_cast<const float*>(p.a) + p.a_off;
+  const float* B = static_cast<const float*>(p.b) + p.b_off;
+  const CUtensorMapDataType F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  CUtensorMap ta, tbm;
+  memset(&ta, 0, sizeof(ta));
+  memset(&tbm, 0, sizeof(tbm));
+  int rc = AMN ? make_map(&ta, A, p.m, p.k, p.batch, p.lda, p.stride_a, BM, 32, F32, 4, CU_TENSOR_MAP_SWIZZLE_NONE)
+               : make_map(&ta, A, p.k, p.m, p.batch, p.lda, p.stride_a, 32, BM, F32, 4, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc != TB_OK) return rc;
+  rc = BMN ? make_map(&tbm, B, p.n, p.k, p.batch, p.ldb, p.stride_b, BN, 32, F32, 4, CU_TENSOR_MAP_SWIZZLE_NONE)
+           : make_map(&tbm, B, p.k, p.n, p.batch, p.ldb, p.stride_b, 32, BN, F32, 4, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc != TB_OK) return rc;
+  const int tiles_m = static_cast<int>((p.m + BM - 1) / BM);
+  const int tiles_n = static_cast<int>((p.n + BN - 1) / BN);
+  const int64_t blocks = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
+  if (blocks > 0x7fffffffLL) return TB_ERR_INVALID;
+  auto kern = sgemm_tma_kernel<BM, BN, 32, TM, TN, ST, AMN, BMN, MINB, XP>;
+  static SmemAttr attr;  // per instantiation, per device
+  if (int rc2 = ensure_smem(attr, kern, Cfg::SMEM_BYTES)) return rc2;
+  dim3 grid(static_cast<unsigned>(blocks)), block(Cfg::NT);
+  kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, cfg_group_m(c, 8));
+  char name[64];
+  snprintf(name, sizeof(name), "sgemm_tma_%dx%dx32_%dx%d_%c%c%s", BM, BN, TM, TN, AMN ? 'm' : 'k', BMN ? 'n' : 'k',
+           (Cfg::A_T || Cfg::B_T) ? "_xp" : "");
+  record(name, grid, block, 1, Cfg::SMEM_BYTES, blocks);
+  return check_launch("sgemm_tma launch");
+}
+
+// Tile families by operand major-ness (a: A M-contiguous, b: B N-contiguous).
+int big_tiles(const Call& c, bool amn, bool bmn) {
+  // K-contiguous operands are transposed in shared memory (XP) so every
+  // layout runs the M/N-contiguous fragment loop: 8192^3 row-major NN
+  // 59.8 -> 63.9, K-contiguous A 58.9 -> 64.5, both 56.7 -> 58.9 TFLOP/s
+  if (amn && bmn) return launch_stma<64, 128, 8, 8, 4, true, true>(c);
+  if (amn) return launch_stma<128, 128, 16, 8, 2, true, false, true>(c);
+  if (bmn) return launch_stma<64, 128, 8, 8, 2, false, true, true>(c);
+  return launch_stma<64, 128, 8, 8, 2, false, false, true>(c);
+}
+int tiles_128x64(const Call& c, bool amn, bool bmn) {
+  if (amn && bmn) return launch_stma<128, 64, 4, 8, 4, true, true>(c);
+  if (amn) return launch_stma<128, 64, 4, 8, 4, true, false>(c);
+  if (bmn) return launch_stma<128, 64, 4, 8, 4, false, true>(c);
+  return -1;  // both K-contiguous: not instantiated (measured slower)
+}
+int tiles_64x64(const Call& c, bool amn, bool bmn) {
+  if (amn && bmn) return launch_stma<64, 64, 4, 8, 3, true, true>(c);
+  if (amn) return launch_stma<64, 64, 4, 8, 3, true, false>(c);
+  if (bmn) return launch_stma<64, 64, 8, 4, 4, false, true>(c);
+  return launch_stma<64, 64, 4, 8, 3, false, false>(c);
+}
+int tiles_64x32(const Call& c, bool amn, bool bmn) {
+  if (amn && bmn) return launch_stma<64, 32, 4, 4, 3, true, true>(c);
+  if (amn) return launch_stma<64, 32, 4, 4, 3, true, false>(c);
+  if (bmn) return launch_stma<64, 32, 4, 4, 3, false, true>(c);
+  return launch_stma<64, 32, 4, 4, 3, false, false>(c);
+}
+int tiles_32x32(const Call& c, bool amn, bool bmn) {
+  // k <= 32 is a single K block: one ring slot and a 51-register cap, so 20
+  // CTAs per SM fit (2 slots at 92 registers: 10; 49.0 -> 44.3 us at S32;
+  // a 42-register cap, 24 CTAs, spills: 47.0 us)
+  if (c.p.k <= 32) {
+    if (amn && bmn) return launch_stma<32, 32, 4, 4, 1, true, true, false, 20>(c);
+    if (amn) return launch_stma<32, 32, 4, 4, 1, true, false, false, 20>(c);
+    if (bmn) return launch_stma<32, 32, 4, 4, 1, false, true, true, 20>(c);
+    return launch_stma<32, 32, 4, 4, 1, false, false, true, 20>(c);
+  }
+  if (amn && bmn) return launch_stma<32, 32, 4, 4, 2, true, true>(c);
+  if (amn) return launch_stma<32, 32, 4, 4, 2, true, false>(c);
+  if (bmn) return launch_stma<32, 32, 4, 4, 2, false, true, true>(c);
+  return launch_stma<32, 32, 4, 4, 2, false, false, true>(c);
+}
+
+}  // namespace
+
+// Route to the TMA kernel: returns -1 when the problem does not qualify.
+// tile: 0 = by shape (built-in routing), 2 = one 64x64 tile per instance
+// (batched 33..64), 3 = one 32x32 tile per instance (batched <= 32),
+// -1 = the configuration's MWG x NWG.
+int dispatch_sgemm_tma(const Call& c, int tile, int mwg, int nwg) {
+  const Problem& p = c.p;
+  const bool amn = !p.a_kcontig, bmn = p.b_ncontig;
+  if (p.a_offs || p.b_offs || p.alphas || p.betas || p.k <= 0 || p.alpha == 0.0f) return -1;
+  if ((p.lda % 4) || (p.ldb % 4) || !aligned_elems(p.a, p.a_off, 4, 16) || !aligned_elems(p.b, p.b_off, 4, 16))
+    return -1;
+  if (p.batch > 1 && ((p.stride_a % 4) || (p.stride_b % 4))) return -1;
+  if (p.m > 0x7fffff00LL || p.n > 0x7fffff00LL || p.k > 0x7fffff00LL || p.batch > 0x7fffffffLL) return -1;
+  if (tile == -1) {
+    if (mwg >= 128 && nwg >= 128) return big_tiles(c, amn, bmn);
+    if (mwg >= 128 && nwg == 64) return tiles_128x64(c, amn, bmn);
+    if (mwg == 64 && nwg == 64) return tiles_64x64(c, amn, bmn);
+    if (mwg == 64 && nwg == 32) return tiles_64x32(c, amn, bmn);
+    if (mwg == 32 && nwg == 32) return tiles_32x32(c, amn, bmn);
+    if (mwg == 64 && nwg >= 128) return big_tiles(c, amn, bmn);
+    return -1;
+  }
+  if (tile == 3) return tiles_32x32(c, amn, bmn);
+  const int sms = sms_or_default();
+  const int64_t tiles128 = ((p.m + 127) / 128) * ((p.n + 127) / 128) * p.batch;
+  // Measured on B200 (tools/sgemm_ms_bench.cu): with >= 4 waves of 128x128
+  // tiles the big tiles win (64x128 8x8 when both operands are M/N-contiguous:
+  // 66 TFLOP/s at 8192^3); below that 64x64 tiles of 4x8 (8x4) micro-tiles
+  // keep every SM busy (1024^3 37.6, C3 (4096,128,9216) 34.8 TFLOP/s).
+  const bool one_tile = p.m <= 64 && p.n <= 64;  // batched small instances: one 64x64 tile each
+  if (tile == 0 && tiles128 >= 4 * sms && !one_tile) return big_tiles(c, amn, bmn);
+  // fewer 64x64 tiles than SMs (e.g. C3 (64, 3136, 576): 49 tiles): 64x32
+  // tiles of 4x4 (21 -> 14 us there; tools/sgemm_ms_bench.cu)
+  const int64_t tiles64 = ((p.m + 63) / 64) * ((p.n + 63) / 64) * p.batch;
+  if (tile == 0 && tiles64 < sms) return tiles_64x32(c, amn, bmn);
+  // 128x64 tiles that fill (nearly) whole waves of one tile per SM: 256
+  // threads of 4x8 beat two 64x64 CTAs per SM by 3-7 % (tools/sgemm_ms_bench.cu:
+  // 1024^3 56 -> 53 us, 1536^3 148 -> 143 us; both-K-contiguous layouts lose)
+  const int64_t tiles128x64 = ((p.m + 127) / 128) * ((p.n + 63) / 64) * p.batch;
+  const int64_t waves = (tiles128x64 + sms - 1) / sms;
+  if (tile == 0 && !one_tile && (amn || bmn) && waves <= 2 && tiles128x64 * 20 >= waves * sms * 17)
+    return tiles_128x64(c, amn, bmn);
+  // batched instances of at most 64x64 with k <= 64 (two K blocks): a
+  // two-slot ring and a 102-register cap, 5 CTAs per SM instead of 4
+  if (one_tile && p.k <= 64) {
+    if (amn && bmn) return launch_stma<64, 64, 4, 8, 2, true, true, false, 5>(c);
+    if (amn) return launch_stma<64, 64, 4, 8, 2, true, false, false, 5>(c);
+    if (bmn) return launch_stma<64, 64, 8, 4, 2, false, true, false, 5>(c);
+    return launch_stma<64, 64, 4, 8, 2, false, false, false, 5>(c);
+  }
+  return tiles_64x64(c, amn, bmn);
+}
+
+}  // namespace host
+}  // namespace tb

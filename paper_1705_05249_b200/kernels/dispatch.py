@@ -16,10 +16,10 @@ import numpy as np
 from ..core import Buffer, Context, Layout, Precision, Transpose
 from ..errors import UsageError
 from . import native
-from .params import Configuration
+from .params import Configuration, is_b200_auto
 
 __all__ = ["gemm_native", "gemm_strided_batched_native", "gemm_batched_native",
-           "prec_code", "require_gpu"]
+           "prec_code", "require_gpu", "b200_config"]
 
 _LAYOUT = {Layout.COL_MAJOR: native.COL_MAJOR, Layout.ROW_MAJOR: native.ROW_MAJOR}
 _TRANS = {Transpose.NO: native.NO_TRANS, Transpose.YES: native.TRANS,
@@ -40,27 +40,43 @@ def require_gpu(ctx: Context) -> None:
         raise native.NativeLibraryError(
             "the GEMM routines run only on a CUDA device (sm_100a); none is visible "
             "— there is no CPU fallback")
+    if not getattr(ctx, "_native_ready", False):
+        # per-device state (wave-barrier counters) allocated once, outside
+        # any graph capture, so no later call allocates
+        import torch
+
+        with torch.cuda.device(ctx.torch_device):
+            native.check(native.lib().tb_prepare_device(), "tb_prepare_device")
+        ctx._native_ready = True
 
 
-_PARAM_STRUCTS: dict = {}
+_CONFIG_STRUCTS: dict = {}
 
 
-def native_config(config: Configuration, source: str) -> Configuration | None:
-    """The configuration the native dispatcher sees: None for the built-in
-    default (the library then picks tiles by shape, from measured crossovers),
-    the configuration itself when it came from an override or the tuning DB
-    (its MWG / NWG / KWG / VW* then select the kernel)."""
-    return None if source == "builtin" else config
+def b200_config(store, precision: Precision, device, args: tuple) -> Configuration | None:
+    """The "gemm_b200" configuration for (m, n, k): an override or an exact
+    tuning-DB entry, else None — the library's built-in shape routing.
+
+    The reference's 14 GemmParams (family "gemm") are validated and recorded
+    in LaunchRecord.params by the routines, but they describe an OpenCL
+    work-group decomposition with no sm_100a meaning and never select a
+    kernel here (DESIGN.md §4 "Tuning space")."""
+    if not store._overrides and (store.database is None or not store.database.entries):
+        return None
+    cfg, source = store.resolve("gemm_b200", precision, device, args)
+    if source == "builtin" or is_b200_auto(cfg):
+        return None
+    return cfg
 
 
 def _params(config: Configuration | None):
     if config is None:
         return None
-    st = _PARAM_STRUCTS.get(config)
+    st = _CONFIG_STRUCTS.get(config)
     if st is None:
-        st = native.TbGemmParams.from_dict(config.as_dict())
-        if len(_PARAM_STRUCTS) < 4096:
-            _PARAM_STRUCTS[config] = st
+        st = native.TbGemmConfig.from_dict(config.as_dict())
+        if len(_CONFIG_STRUCTS) < 4096:
+            _CONFIG_STRUCTS[config] = st
     return ctypes.byref(st)
 
 
@@ -124,12 +140,22 @@ def gemm_batched_native(ctx: Context, precision: Precision, layout: Layout, ta: 
     so = native.lib()
     dev = ctx.torch_device
     batch = int(len(a_offs))
-    # Per-instance arrays travel as device arrays (tbgemm.h: tb_gemm_batched).
-    packed = torch.from_numpy(np.concatenate([
-        np.asarray(a_offs, np.int64), np.asarray(b_offs, np.int64), np.asarray(c_offs, np.int64),
-    ])).to(dev, non_blocking=False)
-    scal = torch.from_numpy(np.concatenate([
-        np.asarray(alphas, np.float32), np.asarray(betas, np.float32)])).to(dev, non_blocking=False)
+    # Per-instance arrays travel as device arrays (tbgemm.h: tb_gemm_batched),
+    # staged through pinned host memory and copied asynchronously on the
+    # call's stream (torch's pinned allocator keeps the staging block alive
+    # until the copy has run).  Host arrays are read at call time, so a CUDA
+    # graph capturing this routine would replay stale offsets: capture
+    # gemm_strided_batched instead.
+    offs_h = torch.empty(3 * batch, dtype=torch.int64, pin_memory=True)
+    o = offs_h.numpy()
+    o[:batch], o[batch:2 * batch], o[2 * batch:] = a_offs, b_offs, c_offs
+    scal_h = torch.empty(2 * batch, dtype=torch.float32, pin_memory=True)
+    sc = scal_h.numpy()
+    sc[:batch], sc[batch:] = alphas, betas
+    stream = torch.cuda.current_stream(dev)
+    with torch.cuda.stream(stream):
+        packed = offs_h.to(dev, non_blocking=True)
+        scal = scal_h.to(dev, non_blocking=True)
     vec = 8 if precision is Precision.H else 4
     aligned = int(all(int(np.all(np.asarray(o) % vec == 0)) for o in (a_offs, b_offs)))
     pa, pb, pc = a.data_ptr(), b.data_ptr(), c.data_ptr()

@@ -19,7 +19,8 @@ from ..errors import TunedBlasError
 
 __all__ = [
     "NativeLibraryError",
-    "TbGemmParams",
+    "TbGemmConfig",
+    "B200_PARAM_NAMES",
     "TbLaunchRecord",
     "lib",
     "library_path",
@@ -59,23 +60,28 @@ EXPORTED_SYMBOLS = (
     "tb_last_error",
     "tb_abi_version",
     "tb_device_sm_count",
+    "tb_prepare_device",
 )
+
+#: Expected TBGEMM_ABI_VERSION (include/tbgemm.h).
+ABI_VERSION = 2
 
 
 class NativeLibraryError(TunedBlasError, RuntimeError):
     """The CUDA library could not be loaded or a kernel launch failed."""
 
 
-_PARAM_NAMES = ("MWG", "NWG", "KWG", "MDIMC", "NDIMC", "MDIMA", "NDIMB",
-                "KWI", "VWM", "VWN", "STRM", "STRN", "SA", "SB")
+#: The "gemm_b200" tuning family (include/tbgemm.h tb_gemm_config;
+#: kernels/params.py), in struct order.
+B200_PARAM_NAMES = ("MWG", "NWG", "KWG", "STAGES", "CTA_GROUP", "SPLIT_K", "GROUP_M")
 
 
-class TbGemmParams(ctypes.Structure):
-    _fields_ = [(name, ctypes.c_int32) for name in _PARAM_NAMES]
+class TbGemmConfig(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_int32) for name in B200_PARAM_NAMES]
 
     @classmethod
-    def from_dict(cls, values: dict) -> "TbGemmParams":
-        return cls(*(int(values[name]) for name in _PARAM_NAMES))
+    def from_dict(cls, values: dict) -> "TbGemmConfig":
+        return cls(*(int(values[name]) for name in B200_PARAM_NAMES))
 
 
 class TbLaunchRecord(ctypes.Structure):
@@ -119,17 +125,17 @@ def _declare(so) -> None:
     so.tb_gemm.restype = _i32
     so.tb_gemm.argtypes = [_i32, _i32, _i32, _i32, _i64, _i64, _i64, _f32,
                            _vp, _i64, _i64, _vp, _i64, _i64, _f32,
-                           _vp, _i64, _i64, _P(TbGemmParams), _i32, _vp]
+                           _vp, _i64, _i64, _P(TbGemmConfig), _i32, _vp]
     so.tb_gemm_strided_batched.restype = _i32
     so.tb_gemm_strided_batched.argtypes = [
         _i32, _i32, _i32, _i32, _i64, _i64, _i64, _f32,
         _vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _f32,
-        _vp, _i64, _i64, _i64, _i64, _P(TbGemmParams), _i32, _vp]
+        _vp, _i64, _i64, _i64, _i64, _P(TbGemmConfig), _i32, _vp]
     so.tb_gemm_batched.restype = _i32
     so.tb_gemm_batched.argtypes = [
         _i32, _i32, _i32, _i32, _i64, _i64, _i64, _vp,
         _vp, _vp, _i64, _vp, _vp, _i64, _vp,
-        _vp, _vp, _i64, _i64, _i32, _P(TbGemmParams), _i32, _vp]
+        _vp, _vp, _i64, _i64, _i32, _P(TbGemmConfig), _i32, _vp]
     so.tb_im2col.restype = _i32
     so.tb_im2col.argtypes = [_i32] + [_i64] * 11 + [_vp, _i64, _vp, _i64, _vp]
     so.tb_transform.restype = _i32
@@ -148,6 +154,8 @@ def _declare(so) -> None:
     so.tb_abi_version.argtypes = []
     so.tb_device_sm_count.restype = _i32
     so.tb_device_sm_count.argtypes = []
+    so.tb_prepare_device.restype = _i32
+    so.tb_prepare_device.argtypes = []
 
 
 def lib():
@@ -167,6 +175,11 @@ def lib():
             except OSError as exc:
                 raise NativeLibraryError(f"cannot load {path}: {exc}") from exc
             _declare(so)
+            ver = so.tb_abi_version()
+            if ver != ABI_VERSION:
+                raise NativeLibraryError(
+                    f"{path} has ABI version {ver}, this package needs {ABI_VERSION}; "
+                    "rebuild with __graft_entry__.build()")
             _lib = so
     return _lib
 

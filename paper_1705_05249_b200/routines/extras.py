@@ -24,7 +24,7 @@ import numpy as np
 from ..core import Buffer, Context, Layout, Precision, Transpose, matrix_span
 from ..errors import UsageError
 from ..kernels import native
-from ..kernels.dispatch import gemm_batched_native, gemm_strided_batched_native, native_config, prec_code
+from ..kernels.dispatch import b200_config, gemm_batched_native, gemm_strided_batched_native, prec_code
 from ..kernels.engine import WorkGrid, pre_launch, record_launch, reference_grid
 from .common import check_precision, get_store, scalars, stored_dims
 from .level3 import route_family
@@ -116,10 +116,10 @@ def _validate(ctx, layout, trans_a, trans_b, m, n, k, a, a_offs, lda, b, b_offs,
 
 def _launch_family(ctx, precision, m, n, k):
     store = get_store(ctx)
-    cfg, source = store.resolve("gemm", precision, ctx.device, (m, n, k))
+    cfg, _ = store.resolve("gemm", precision, ctx.device, (m, n, k))
     route = route_family(m, n, k, store.direct_threshold, None)
     family = "gemm_direct" if route == "direct" else "gemm"
-    return cfg, family, native_config(cfg, source)
+    return cfg, family, b200_config(store, precision, ctx.device, (m, n, k))
 
 
 def gemm_batched(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Transpose,
@@ -154,7 +154,7 @@ def gemm_batched(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Tran
     if computes:
         # All-alpha-zero batches make no launch in the reference
         # (extras.py:281-286), so last_launch is left unchanged then.
-        record_launch(ctx, family, cfg, grid, launched)
+        record_launch(ctx, family, cfg, grid, launched, ncfg)
 
 
 def gemm_strided_batched(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Transpose,
@@ -203,4 +203,4 @@ def gemm_strided_batched(ctx: Context, layout: Layout, trans_a: Transpose, trans
         a, a_offset, lda_e, stride_a, b, b_offset, ldb_e, stride_b, float(be),
         c, c_offset, ldc_e, stride_c, batch_count, ncfg, native.FLAG_TF32 if tf32 else 0)
     if computes:
-        record_launch(ctx, family, cfg, grid, launched)
+        record_launch(ctx, family, cfg, grid, launched, ncfg)

@@ -14,7 +14,7 @@ from __future__ import annotations
 from ..core import Buffer, Context, Layout, Precision, Transpose
 from ..errors import UsageError
 from ..kernels import native
-from ..kernels.dispatch import gemm_native, native_config, prec_code
+from ..kernels.dispatch import b200_config, gemm_native, prec_code
 from ..kernels.engine import pre_launch, record_launch, reference_grid
 from .common import check_logical, check_precision, default_ld, get_store, scalar, stored_dims
 
@@ -82,13 +82,13 @@ def gemm(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Transpose,
                     a, a_offset, lda, b, b_offset, ldb, beta, c, c_offset, ldc, None)
         return
 
-    cfg, source = store.resolve("gemm", precision, ctx.device, (m, n, k))
+    cfg, _ = store.resolve("gemm", precision, ctx.device, (m, n, k))
     route = route_family(m, n, k, store.direct_threshold, kernel)
     family = "gemm_direct" if route == "direct" else "gemm"
     grid = reference_grid(family, m, n, cfg)
     pre_launch(ctx, family, cfg, grid, precision)
+    kcfg = b200_config(store, precision, ctx.device, (m, n, k))
     launched = gemm_native(ctx, precision, layout, trans_a, trans_b, m, n, k, alpha,
-                           a, a_offset, lda, b, b_offset, ldb, beta, c, c_offset, ldc,
-                           native_config(cfg, source),
+                           a, a_offset, lda, b, b_offset, ldb, beta, c, c_offset, ldc, kcfg,
                            route_flags(kernel) | (native.FLAG_TF32 if tf32 else 0))
-    record_launch(ctx, family, cfg, grid, launched)
+    record_launch(ctx, family, cfg, grid, launched, kcfg)

@@ -25,7 +25,7 @@ from ..core import (Buffer, Context, Diagonal, Layout, Precision, Side, Transpos
                     buffer_from_tensor, check_matrix)
 from ..errors import SingularMatrixError, UsageError
 from ..kernels import native
-from ..kernels.dispatch import gemm_native, prec_code, require_gpu, native_config
+from ..kernels.dispatch import b200_config, gemm_native, prec_code, require_gpu
 from .common import check_logical, check_precision, get_store, scalar
 from .level3 import gemm
 
@@ -354,7 +354,7 @@ def trsm(ctx: Context, layout: Layout, side: Side, triangle: Triangle,
     C = Layout.COL_MAJOR
     # Panel updates go straight to the C-ABI (their operands are this
     # routine's own validated temps); FP32 built-in configuration.
-    cfg = native_config(*get_store(ctx).resolve("gemm", S, ctx.device, (na, xc, nb)))
+    cfg = b200_config(get_store(ctx), S, ctx.device, (na, xc, nb))
     unit = int(diagonal is Diagonal.UNIT)
 
     def update(r0, r1, k0, k1):

@@ -7,10 +7,17 @@ tuner.py:44-358): explore the valid curated set (params.py:221-243) plus
 (status "failed" on mismatch or exception), then 1 warm-up + 10 timed runs;
 best = lowest mean, then fewest threads, then lexicographic parameters.
 
-What changes on the B200: each candidate runs the sm_100a instantiation its
-parameters map to (kernels/params.py), every run is timed with CUDA events
-on the launching stream, inputs stay resident in HBM, and the oracle is a
-float64 product computed on the device with the exact tolerance bound.
+What changes on the B200: the family that selects kernels is
+``gemm_b200`` (kernels/params.py; include/tbgemm.h tb_gemm_config) — CTA
+tile MWG x NWG, K depth per stage KWG, ring depth STAGES, tcgen05
+CTA_GROUP, cluster SPLIT_K and raster GROUP_M — whose curated set is the
+built-in shape route followed by every instantiated kernel of the precision
+under each curated GROUP_M, so the tuned best is never slower than the
+untuned default.  Every run is timed with CUDA events on the launching
+stream, inputs stay resident in HBM, and the oracle is a float64 product
+computed on the device with the exact tolerance bound.  The reference's
+14-parameter ``gemm`` family can still be tuned (same protocol; its
+configurations are validated and recorded but select no kernel on sm_100a).
 """
 
 from __future__ import annotations
@@ -25,7 +32,9 @@ from .errors import TuningError, UsageError
 from .kernels.dispatch import gemm_native
 from .kernels.params import (
     Configuration,
+    curated_b200,
     curated_configurations,
+    is_b200_auto,
     random_configuration,
     validate_config,
     work_group_threads,
@@ -121,7 +130,7 @@ class _KernelHarness:
     def __init__(self, task: TuningTask, ctx: Context):
         import torch
 
-        if task.kernel_family != "gemm":
+        if task.kernel_family not in ("gemm", "gemm_b200"):
             raise UsageError(f"unknown kernel family {task.kernel_family!r}")
         m, n, k = task.sizes()
         if m < 1 or n < 1 or k < 1:
@@ -146,9 +155,12 @@ class _KernelHarness:
 
     def run(self, cfg: Configuration):
         t = self.task
+        # only gemm_b200 configurations select a kernel (the all-zero one is
+        # the built-in shape route); reference configurations are recorded only
+        kcfg = cfg if cfg.family == "gemm_b200" and not is_b200_auto(cfg) else None
         launched = gemm_native(self.ctx, t.precision, Layout.COL_MAJOR, Transpose.NO, Transpose.NO,
                                self.m, self.n, self.k, 1.0, self.abuf, 0, self.m,
-                               self.bbuf, 0, self.k, 0.0, self.cbuf, 0, self.m, cfg)
+                               self.bbuf, 0, self.k, 0.0, self.cbuf, 0, self.m, kcfg)
         self.last_kernel = launched["kernel"]
         return self.cbuf
 
@@ -196,7 +208,9 @@ def tune(task: TuningTask, ctx: Context) -> TuningRun:
     harness = _KernelHarness(task, ctx)
     explored: list[Configuration] = []
     seen = set()
-    for cfg in curated_configurations(task.kernel_family):
+    curated = (curated_b200(task.precision) if task.kernel_family == "gemm_b200"
+               else curated_configurations(task.kernel_family))
+    for cfg in curated:
         if validate_config(cfg, task.device, task.precision) and cfg not in seen:
             explored.append(cfg)
             seen.add(cfg)
@@ -219,8 +233,16 @@ def tune(task: TuningTask, ctx: Context) -> TuningRun:
     return TuningRun(task=task, measurements=measurements, best=_select_best(ok))
 
 
+def _tie_break(cfg: Configuration) -> int:
+    """Second key after the mean time: fewest threads (reference,
+    tuner.py:344-349); for gemm_b200 the built-in route wins ties."""
+    if cfg.family == "gemm_b200":
+        return 0 if is_b200_auto(cfg) else 1
+    return work_group_threads(cfg)
+
+
 def _select_best(ok_measurements) -> Configuration:
-    return min(ok_measurements, key=lambda m: (m.mean_time, work_group_threads(m.configuration),
+    return min(ok_measurements, key=lambda m: (m.mean_time, _tie_break(m.configuration),
                                                m.configuration.values)).configuration
 
 

@@ -24,13 +24,14 @@ def test_library_exports_every_symbol():
     so = native.lib()
     for name in declared_functions():
         assert hasattr(so, name), name
-    assert so.tb_abi_version() == 1
+    assert so.tb_abi_version() == native.ABI_VERSION == 2
     assert so.tb_status_str(0) == b"ok"
     assert so.tb_status_str(3) == b"unsupported"
 
 
 def test_struct_layouts():
-    assert ctypes.sizeof(native.TbGemmParams) == 14 * 4
+    assert ctypes.sizeof(native.TbGemmConfig) == 7 * 4
+    assert [f for f, _ in native.TbGemmConfig._fields_] == list(native.B200_PARAM_NAMES)
     assert ctypes.sizeof(native.TbLaunchRecord) == 64 + 24 + 12 + 12 + 4 + 4 + 8
 
 

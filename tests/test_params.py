@@ -97,3 +97,41 @@ def test_launch_grid_examples():
     with pytest.raises(tb.UsageError):
         tb.launch_grid("gemm", (100, 128), cfg)
     assert tb.launch_grid("gemm_direct", (100, 70), cfg).work_groups == (2, 2)
+
+
+def test_gemm_b200_family():
+    """The sm_100a tuning family: instantiated kernels only, the all-zero
+    built-in route first in the curated list, sm_100 devices only."""
+    from paper_1705_05249_b200.kernels.params import (b200_auto, b200_variants, curated_b200,
+                                                      is_b200_auto, validate_config)
+
+    B200 = tb.b200_device()
+    for prec in (Precision.H, Precision.S):
+        cur = curated_b200(prec)
+        assert is_b200_auto(cur[0]) and len(set(cur)) == len(cur)
+        assert all(validate_config(c, B200, prec) for c in cur)
+        assert len(cur) == 1 + 4 * len(b200_variants(prec))
+    assert validate_config(b200_auto(), B200, Precision.S)
+    bad = tb.Configuration.make("gemm_b200", dict(MWG=256, NWG=256, KWG=64, STAGES=0, CTA_GROUP=2,
+                                                  SPLIT_K=1, GROUP_M=0))
+    assert validate_config(bad, B200, Precision.H) and not validate_config(bad, B200, Precision.S)
+    host = tb.DeviceSpec()
+    assert not validate_config(b200_auto(), host, Precision.S)
+
+
+def test_gemm_b200_exact_only_resolution():
+    """gemm_b200 DB entries apply to their exact shape only (tuningdb.py
+    EXACT_ONLY_FAMILIES); other shapes fall back to the built-in route."""
+    from paper_1705_05249_b200.kernels.params import curated_b200, is_b200_auto
+    from paper_1705_05249_b200.tuningdb import DbEntry, DbKey
+
+    B200 = tb.b200_device()
+    cfg = curated_b200(Precision.H)[5]
+    db = tb.Database()
+    key = DbKey.for_task("gemm_b200", Precision.H, B200, (4096, 128, 9216))
+    db.insert(DbEntry(key=key, measurements=[{"params": cfg.as_dict(), "per_run_times_s": [1e-5],
+                                              "mean_time_s": 1e-5, "status": "ok"}], best=cfg))
+    store = tb.ParameterStore(database=db)
+    assert store.resolve("gemm_b200", Precision.H, B200, (4096, 128, 9216)) == (cfg, "device")
+    got, src = store.resolve("gemm_b200", Precision.H, B200, (1024, 1024, 1024))
+    assert is_b200_auto(got) and src == "builtin"

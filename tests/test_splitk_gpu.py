@@ -154,13 +154,22 @@ def test_splitk_deterministic(ctx):
 
 
 def test_no_split_for_large_or_short_k(ctx):
+    """Routing: no split for a square 2048^3 or the short-K C3 shape
+    (64, 3136, 576); results on random data within the FP16 tolerance."""
     import torch
 
     prec = Precision.H
     for (m, n, k) in ((2048, 2048, 2048), (64, 3136, 576)):
-        a = tb.buffer_from_tensor(ctx, prec, torch.zeros(m * k, device="cuda").half())
-        b = tb.buffer_from_tensor(ctx, prec, torch.zeros(k * n, device="cuda").half())
+        g = torch.Generator(device="cuda").manual_seed(m + n + k)
+        at = (torch.rand(m * k, device="cuda", generator=g) * 2 - 1).half()
+        bt = (torch.rand(k * n, device="cuda", generator=g) * 2 - 1).half()
+        a, b = tb.buffer_from_tensor(ctx, prec, at), tb.buffer_from_tensor(ctx, prec, bt)
         c = tb.buffer_alloc(ctx, prec, m * n)
         tb.gemm(ctx, Layout.ROW_MAJOR, Transpose.NO, Transpose.NO, m, n, k, 1.0, a, b, 0.0, c)
         assert "splitk" not in ctx.last_launch.native["kernel"], (m, n, k, ctx.last_launch.native)
-        assert np.all(tb.buffer_read(c, 0, m * n) == 0)
+        A, B = at.view(m, k).double(), bt.view(k, n).double()
+        want = A @ B
+        tol = 4 * 2.0 ** -10 * k * A.abs().amax(1, keepdim=True) * B.abs().amax(0, keepdim=True) \
+            + 2.0 ** -11 * want.abs()
+        got = c.device_tensor().view(m, n).double()
+        assert bool(((got - want).abs() <= tol).all())
