@@ -167,6 +167,22 @@ class _KernelHarness:
     def result(self):
         return self.cbuf.device_tensor().view(self.n, self.m).t()
 
+    def prewarm(self, cfg: Configuration, seconds: float = 0.05) -> None:
+        """Run ``cfg`` back to back for ~``seconds`` of device time before the
+        first measurement, so the first candidate (the built-in route) is not
+        timed on a GPU still ramping its clocks up from idle."""
+        import torch
+
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(self.ctx.stream)
+        self.run(cfg)
+        t1.record(self.ctx.stream)
+        t1.synchronize()
+        reps = int(min(10000, max(1, seconds * 1e3 / max(t0.elapsed_time(t1), 1e-3))))
+        for _ in range(reps):
+            self.run(cfg)
+        self.ctx.stream.synchronize()
+
     def verify(self, cfg: Configuration) -> bool:
         self.run(cfg)
         return device_within_tol(self.result(), self.expected, self.tol)
@@ -225,6 +241,8 @@ def tune(task: TuningTask, ctx: Context) -> TuningRun:
         explored.append(cand)
         seen.add(cand)
         accepted += 1
+    if explored:
+        harness.prewarm(explored[0])
     measurements = [measure(cfg, task, ctx, harness) for cfg in explored]
     ok = [m for m in measurements if m.status == "ok"]
     if not ok:

@@ -113,10 +113,11 @@ def test_baseline_config_parity(ctx, case):
 
 
 @pytest.mark.parametrize("size", [1024, 1536])
-@pytest.mark.parametrize("ta,tbn", [("n", "n"), ("n", "t"), ("t", "n")])
+@pytest.mark.parametrize("ta,tbn", [("n", "n"), ("t", "n"), ("t", "t")])
 def test_sgemm_128x64_route(ctx, size, ta, tbn):
-    """The 128x64 TMA SGEMM (the kernel serving C1) in each layout it takes:
-    bitwise against the sequential-k oracle on sampled rows."""
+    """The 128x64 TMA SGEMM (the kernel serving C1) in each layout it takes
+    (row-major: op(B) N-contiguous or op(A) M-contiguous, i.e. every (ta, tb)
+    but (N, T)): bitwise against the sequential-k oracle on sampled rows."""
     import torch
 
     m = n = k = size

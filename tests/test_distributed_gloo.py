@@ -76,3 +76,51 @@ def test_gather_replicates_c_world2(n_cols):
     for p in procs:
         p.join(timeout=60)
     assert results == {0: True, 1: True}
+
+
+def _chunk_worker(rank, world, port, n_rows, chunks, q):
+    """Row-major C (M shards): each rank fills its rows sub-block by sub-block
+    and replicates every sub-block with send_chunk as soon as it is 'computed'
+    (the overlapped replicate_c path of gemm_sharded)."""
+    from paper_1705_05249_b200.distributed import chunk_ranges, send_chunk
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, k = 5, 4
+        rng = np.random.default_rng(1)
+        A = rng.standard_normal((n_rows, k)).astype(np.float32)
+        B = rng.standard_normal((k, n)).astype(np.float32)
+        want = (A @ B).reshape(-1)                         # row-major C
+        plan = plan_gemm_shards(Layout.ROW_MAJOR, n_rows, n, world)
+        s0, cnt = plan.of(rank)
+        c = torch.full((n_rows * n,), -1.0, dtype=torch.float32)
+        works = []
+        parts = chunk_ranges(cnt, chunks)
+        for j, (o, sz) in enumerate(parts):
+            u0 = s0 + o
+            c[u0 * n:(u0 + sz) * n] = torch.from_numpy(want[u0 * n:(u0 + sz) * n])
+            works += send_chunk(c, plan, rank, n, j, chunks)
+        for j in range(len(parts), max(len(chunk_ranges(pc, chunks)) for pc in plan.counts)):
+            works += send_chunk(c, plan, rank, n, j, chunks)
+        for w in works:
+            w.wait()
+        q.put((rank, bool(np.array_equal(c.numpy(), want))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_rows,chunks", [(2, 8, 2), (2, 7, 3), (3, 7, 4), (3, 2, 2)])
+def test_chunked_replication(world, n_rows, chunks):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chunk_worker, args=(r, world, port, n_rows, chunks, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert results == {r: True for r in range(world)}

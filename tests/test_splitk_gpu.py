@@ -63,7 +63,7 @@ def test_c3_shape_splits_and_is_accurate(ctx, layout, ta, tbn):
     m, n, k = 4096, 128, 9216
     at, bt, a, b, (ar, ac, lda), (br, bc, ldb) = _operands(ctx, m, n, k, ta, tbn, layout, seed=11)
     ldc = m if layout == "col" else n
-    cfg = tb.routines.common.get_store(ctx).resolve("gemm", Precision.H, ctx.device, (m, n, k))[0]
+    cfg = None  # built-in shape routing (gemm_b200 configurations select kernels)
     outs, kernels = [], []
     for flags in (0, native.FLAG_NO_TMA, native.FLAG_NO_SPLITK):
         c = tb.buffer_alloc(ctx, Precision.H, m * n)
@@ -98,7 +98,7 @@ def test_splitk_ragged_beta_and_offsets(ctx):
     g = torch.Generator(device="cuda").manual_seed(9)
     c0 = (torch.rand(ldc * n + 16, device="cuda", generator=g) * 2 - 1).half()
     c = tb.buffer_from_tensor(ctx, Precision.H, c0.clone())
-    cfg = tb.routines.common.get_store(ctx).resolve("gemm", Precision.H, ctx.device, (m, n, k))[0]
+    cfg = None  # built-in shape routing (gemm_b200 configurations select kernels)
     rec = gemm_native(ctx, Precision.H, L[layout], T[ta], T[tbn], m, n, k, 1.5, a, 0, lda, b, 0, ldb,
                       -0.5, c, 8, ldc, cfg, 0)
     assert "splitk" in rec["kernel"], rec
