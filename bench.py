@@ -3,15 +3,18 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--workload hgemm|sgemm|batched_h32|batched_s32|batched_h64|batched_s64|
-                                sgemm_c1|hgemm_c3|sgemm_c3|hgemm_c5|sgemm_c5]
-                    [--no-extra] [--no-cpu-baseline]
+                                sgemm_c1|hgemm_c3|sgemm_c3|hgemm_c3b|sgemm_c3b|hgemm_c5|sgemm_c5]
+                    [--replicate-c] [--chunks C] [--no-extra] [--no-cpu-baseline]
+                    [--sweep-out PATH]
 
 A "step" is one call of the hot path on one batch of synthetic input:
 * hgemm (default, the headline): C = A·B, 8192^3, FP16 storage / FP32
   accumulate, row-major NN, alpha=1, beta=0 (BASELINE configs[1], largest
   square size of the sweep);
 * sgemm: the same shape in FP32 (FFMA);
-* batched_*: gemm_strided_batched, 16384 instances of 32^3 / 64^3 (configs[3]).
+* batched_*: gemm_strided_batched, 16384 instances of 32^3 / 64^3 (configs[3]);
+* sgemm_c1: 1024^3 (configs[0]); *_c3 / *_c3b: (4096,128,9216) / (64,3136,576)
+  (configs[2]); *_c5: 32768^3 (configs[4]).
 
 value   = whole-job GFLOPS with inputs resident in HBM, CUDA-event timed per
           step on the launching stream (max over ranks), L2 flushed between
@@ -19,9 +22,16 @@ value   = whole-job GFLOPS with inputs resident in HBM, CUDA-event timed per
 e2e     = the same metric through the public API with HOST buffers: pinned
           host → device copy of A and B, the routine, device → host copy of C,
           all inside the timed region.
-N > 1   = weak scaling: rank r computes its own 8192-column block of an
-          8192 x (8192·N) x 8192 GEMM (column-sharded C, no collective) or its
-          own 16384-instance block of the batch.
+N > 1   = every rank runs the library's sharding (paper_1705_05249_b200/
+          distributed.py) one process per GPU over NCCL:
+          * gemm workloads: weak scaling — rank r computes its M-block (row-major
+            C) of an (m·N) x n x k GEMM through ``gemm_sharded``;
+          * *_c5: strong scaling — the fixed 32768^3 GEMM split into N row
+            blocks through ``gemm_sharded``;
+          * batched: weak scaling — N·16384 instances, rank r its contiguous
+            16384 through ``gemm_strided_batched_sharded``;
+          * --replicate-c adds the replication of C to every rank inside the
+            timed step (--chunks C > 1: overlapped per-sub-block transfers).
 --impl reference times the reference's CPU implementation of the path (the
 oracle port of tunedblas' tiled algorithm, oracle/gemm_oracle.py) on the
 host cores, each step a bounded row-block sample of the same workload.
@@ -66,8 +76,11 @@ WORKLOADS = {
     "sgemm_c1": dict(kind="gemm", prec="S", m=1024, n=1024, k=1024, batch=1),
     "hgemm_c3": dict(kind="gemm", prec="H", m=4096, n=128, k=9216, batch=1),
     "sgemm_c3": dict(kind="gemm", prec="S", m=4096, n=128, k=9216, batch=1),
-    # C5: the large GEMM (per rank under torchrun: weak scaling, each rank its
-    # own 32768-column block)
+    # C3's other im2col'd layer (64, 3136, 576)
+    "hgemm_c3b": dict(kind="gemm", prec="H", m=64, n=3136, k=576, batch=1),
+    "sgemm_c3b": dict(kind="gemm", prec="S", m=64, n=3136, k=576, batch=1),
+    # C5: the large GEMM (under torchrun: strong scaling, the fixed problem
+    # split into N row blocks)
     "hgemm_c5": dict(kind="gemm", prec="H", m=32768, n=32768, k=32768, batch=1),
     "sgemm_c5": dict(kind="gemm", prec="S", m=32768, n=32768, k=32768, batch=1),
 }
@@ -153,33 +166,86 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def make_operands(tb, ctx, w, rank, world, torch):
+def is_strong(name: str) -> bool:
+    """C5 is strong-scaled (the fixed 32768^3 problem split over the ranks);
+    every other workload is weak-scaled (per-rank work fixed)."""
+    return name.endswith("_c5")
+
+
+def shard_of(w: dict, name: str, world: int, rank: int) -> dict:
+    """The whole job's problem and this rank's share of it: row blocks of a
+    row-major C for gemm (distributed.plan_gemm_shards), contiguous instance
+    blocks for batched (distributed.gemm_strided_batched_sharded)."""
+    from paper_1705_05249_b200.distributed import shard_range
+
+    if w["kind"] == "gemm":
+        M = w["m"] if is_strong(name) else w["m"] * world
+        s0, cnt = shard_range(M, world, rank)
+        return dict(M=M, batch=1, s0=s0, cnt=cnt)
+    total = w["batch"] * world
+    s0, cnt = shard_range(total, world, rank)
+    return dict(M=w["m"], batch=total, s0=s0, cnt=cnt)
+
+
+def job_flops(w: dict, sh: dict) -> float:
+    if w["kind"] == "gemm":
+        return 2.0 * sh["M"] * w["n"] * w["k"]
+    return 2.0 * w["m"] * w["n"] * w["k"] * sh["batch"]
+
+
+def rank_flops(w: dict, sh: dict) -> float:
+    if w["kind"] == "gemm":
+        return 2.0 * sh["cnt"] * w["n"] * w["k"]
+    return 2.0 * w["m"] * w["n"] * w["k"] * sh["cnt"]
+
+
+def rank_bytes(w: dict, sh: dict) -> float:
+    es = 2 if w["prec"] == "H" else 4
+    if w["kind"] == "gemm":
+        return (sh["cnt"] * w["k"] + w["k"] * w["n"] + sh["cnt"] * w["n"]) * es
+    return (w["m"] * w["k"] + w["k"] * w["n"] + w["m"] * w["n"]) * es * sh["cnt"]
+
+
+def make_operands(tb, ctx, w, sh, torch):
+    """Whole-job buffers; only this rank's rows / instances (and, for gemm,
+    the replicated B) are filled: U(-1, 1), seeded per rank."""
     prec = tb.Precision.H if w["prec"] == "H" else tb.Precision.S
     dt = prec.torch_dtype
     dev = ctx.torch_device
-    g = torch.Generator(device=dev).manual_seed(12345 + rank)
+    g = torch.Generator(device=dev).manual_seed(12345 + sh["s0"])
     if w["kind"] == "gemm":
-        m, n, k = w["m"], w["n"], w["k"]
-        # rank's column block of an m x (n*world) x k GEMM: A (m x k) replicated,
-        # B block (k x n) and C block (m x n) local — row-major packed.
-        na, nb, nc = m * k, k * n, m * n
+        m_all, n, k = sh["M"], w["n"], w["k"]
+        na, nb, nc = m_all * k, k * n, m_all * n
+        a_lo, a_hi = sh["s0"] * k, (sh["s0"] + sh["cnt"]) * k
+        b_lo, b_hi = 0, nb
     else:
         e = w["m"] * w["k"]
-        na = nb = nc = e * w["batch"]
-    at = (torch.rand(na, device=dev, generator=g) * 2 - 1).to(dt)
-    bt = (torch.rand(nb, device=dev, generator=g) * 2 - 1).to(dt)
+        na = nb = nc = e * sh["batch"]
+        a_lo, a_hi = sh["s0"] * e, (sh["s0"] + sh["cnt"]) * e
+        b_lo, b_hi = a_lo, a_hi
+    at = torch.zeros(na, device=dev, dtype=dt)
+    bt = torch.zeros(nb, device=dev, dtype=dt)
+    at[a_lo:a_hi] = (torch.rand(a_hi - a_lo, device=dev, generator=g) * 2 - 1).to(dt)
+    bt[b_lo:b_hi] = (torch.rand(b_hi - b_lo, device=dev, generator=g) * 2 - 1).to(dt)
     ct = torch.zeros(nc, device=dev, dtype=dt)
     return prec, tb.buffer_from_tensor(ctx, prec, at), tb.buffer_from_tensor(ctx, prec, bt), \
         tb.buffer_from_tensor(ctx, prec, ct)
 
 
-def step_fn(tb, ctx, w, prec, a, b, c):
+def step_fn(tb, ctx, w, sh, a, b, c, rank, world, replicate_c=False, chunks=1):
+    """One step = this rank's share through the library's sharding (a plain
+    gemm / gemm_strided_batched call at N = 1)."""
+    from paper_1705_05249_b200 import distributed as D
+
     L, T = tb.Layout.ROW_MAJOR, tb.Transpose.NO
     if w["kind"] == "gemm":
-        m, n, k = w["m"], w["n"], w["k"]
-        return lambda: tb.gemm(ctx, L, T, T, m, n, k, 1.0, a, b, 0.0, c)
-    m, e, bt = w["m"], w["m"] * w["m"], w["batch"]
-    return lambda: tb.gemm_strided_batched(ctx, L, T, T, m, m, m, 1.0, a, e, b, e, 0.0, c, e, bt)
+        M, n, k = sh["M"], w["n"], w["k"]
+        return lambda: D.gemm_sharded(ctx, L, T, T, M, n, k, 1.0, a, b, 0.0, c, rank=rank, world=world,
+                                      replicate_c=replicate_c, chunks=chunks)
+    s, e, total = w["m"], w["m"] * w["m"], sh["batch"]
+    return lambda: D.gemm_strided_batched_sharded(ctx, L, T, T, s, s, s, 1.0, a, e, b, e, 0.0, c, e, total,
+                                                  rank=rank, world=world, replicate_c=replicate_c,
+                                                  chunks=chunks)
 
 
 def device_time(fn, steps, warmup, stream, torch, flush):
@@ -199,12 +265,35 @@ def device_time(fn, steps, warmup, stream, torch, flush):
     return [e0.elapsed_time(e1) / 1e3 for e0, e1 in evs]
 
 
+def roofline_of(w, per_launch, peaks, peak_src, sh):
+    """Bound, peak and achieved for the dominant kernel of one rank's step."""
+    fl, by = rank_flops(w, sh), rank_bytes(w, sh)
+    ai = fl / by
+    ridge = (peaks["bf16_tflops"] if w["prec"] == "H" else FFMA_TFLOPS) * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    if w["kind"] == "gemm" and ai < ridge:
+        bound, peak, unit, achieved = "hbm", peaks["hbm_gbs"], "GB/s", by / per_launch / 1e9
+        note = (f"HBM copy bandwidth ({peak_src}: MEASURED_PEAKS.json hbm_gbs); "
+                f"arithmetic intensity {ai:.0f} flop/B < ridge {ridge:.0f}")
+    elif w["prec"] == "H" and w["kind"] == "gemm":
+        bound, peak, unit, achieved = "tensor", peaks["bf16_tflops"], "TFLOP/s", fl / per_launch / 1e12
+        note = f"dense FP16/BF16 tensor, burst ({peak_src}: MEASURED_PEAKS.json bf16_tflops)"
+    elif w["kind"] == "gemm":
+        bound, peak, unit, achieved = "ffma", FFMA_TFLOPS, "TFLOP/s", fl / per_launch / 1e12
+        note = "FP32 FFMA 148 SM x 128 lanes x 2 x 1.965 GHz (derived, no measured FFMA peak)"
+    else:
+        bound, peak, unit, achieved = "hbm", peaks["hbm_gbs"], "GB/s", by / per_launch / 1e9
+        note = f"HBM copy bandwidth ({peak_src}: MEASURED_PEAKS.json hbm_gbs)"
+    return {"bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
+            "frac": round(achieved / peak, 4), "traffic": None, "peak_source": note,
+            "per_launch_ms": round(per_launch * 1e3, 4),
+            "algorithmic": f"{fl:.4g} FLOP, {by:.4g} B per launch"}
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
     import paper_1705_05249_b200 as tb
-    from paper_1705_05249_b200.kernels import native
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -223,10 +312,18 @@ def run_ours(args, rank, world, local_rank):
         clean_buf.view(torch.int64).sum()
     peaks, peak_src = load_peaks()
 
-    def measure(name, steps, warmup):
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def measure(name, steps, warmup, replicate_c=False, chunks=1):
         w = WORKLOADS[name]
-        prec, a, b, c = make_operands(tb, ctx, w, rank, world, torch)
-        fn = step_fn(tb, ctx, w, prec, a, b, c)
+        sh = shard_of(w, name, world, rank)
+        prec, a, b, c = make_operands(tb, ctx, w, sh, torch)
+        fn = step_fn(tb, ctx, w, sh, a, b, c, rank, world, replicate_c, chunks)
         fn()
         torch.cuda.synchronize()
         kernel = ctx.last_launch.native["kernel"]
@@ -236,113 +333,21 @@ def run_ours(args, rank, world, local_rank):
         sampler = ClockSampler(local_rank)
         with sampler:
             times = device_time(fn, steps, warmup, stream, torch, flush)
-        total = sum(times)
-        if world > 1:
-            t = torch.tensor([total], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            total = float(t.item())
-        per_launch = total / steps
-        gflops = flops(w) * world * steps / total / 1e9
-        ai = flops(w) / alg_bytes(w)
-        ridge = (peaks["bf16_tflops"] if w["prec"] == "H" else FFMA_TFLOPS) * 1e12 / (peaks["hbm_gbs"] * 1e9)
-        if w["kind"] == "gemm" and ai < ridge:
-            bound = "hbm"
-            peak, unit, achieved = peaks["hbm_gbs"], "GB/s", alg_bytes(w) / per_launch / 1e9
-            peak_note = (f"HBM copy bandwidth ({peak_src}: MEASURED_PEAKS.json hbm_gbs); "
-                         f"arithmetic intensity {ai:.0f} flop/B < ridge {ridge:.0f}")
-        elif w["prec"] == "H" and w["kind"] == "gemm":
-            bound = "tensor"
-            peak, unit, achieved = peaks["bf16_tflops"], "TFLOP/s", flops(w) / per_launch / 1e12
-            peak_note = f"dense FP16/BF16 tensor, burst ({peak_src}: MEASURED_PEAKS.json bf16_tflops)"
-        elif w["kind"] == "gemm":
-            bound = "ffma"
-            peak, unit, achieved = FFMA_TFLOPS, "TFLOP/s", flops(w) / per_launch / 1e12
-            peak_note = "FP32 FFMA 148 SM x 128 lanes x 2 x 1.965 GHz (derived, no measured FFMA peak)"
-        else:
-            bound = "hbm"
-            peak, unit, achieved = peaks["hbm_gbs"], "GB/s", alg_bytes(w) / per_launch / 1e9
-            peak_note = f"HBM copy bandwidth ({peak_src}: MEASURED_PEAKS.json hbm_gbs)"
-        return dict(name=name, w=w, times=times, total=total, gflops=gflops, kernel=kernel,
-                    clocks=sampler.summary(), a=a, b=b, c=c, prec=prec, fn=fn,
-                    roofline={"bound": bound, "achieved": round(achieved, 2), "peak": peak,
-                              "unit": unit, "frac": round(achieved / peak, 4),
-                              "traffic": None, "peak_source": peak_note,
-                              "kernel": kernel, "per_launch_ms": round(per_launch * 1e3, 4),
-                              "algorithmic": f"{flops(w):.4g} FLOP, {alg_bytes(w):.4g} B per launch"})
+        total = max_over_ranks(sum(times))
+        per_launch = sum(times) / steps
+        gflops = job_flops(w, sh) * steps / total / 1e9
+        roof = roofline_of(w, per_launch, peaks, peak_src, sh)
+        roof["kernel"] = kernel
+        return dict(name=name, w=w, sh=sh, times=times, total=total, gflops=gflops, kernel=kernel,
+                    clocks=sampler.summary(), a=a, b=b, c=c, prec=prec, fn=fn, roofline=roof)
 
-    main = measure(args.workload, args.steps, args.warmup)
-    w = main["w"]
+    main = measure(args.workload, args.steps, args.warmup, args.replicate_c, args.chunks)
+    w, sh = main["w"], main["sh"]
 
-    # ---- e2e: public API with host buffers, copies inside the timed region ----
-    # Every step copies its A and B from pinned host memory, runs the routine
-    # and copies C back.  Steps are software-pipelined over three streams
-    # (H2D copy engine, compute, D2H copy engine) with double-buffered device
-    # operands, so step i's D2H and step i+1's H2D overlap (PCIe is full
-    # duplex) — the copies of every step stay inside the timed region.
-    prec, a, b, c = main["prec"], main["a"], main["b"], main["c"]
-    dt = prec.torch_dtype
-    host_a = torch.empty(a.length, dtype=dt, pin_memory=True)
-    host_b = torch.empty(b.length, dtype=dt, pin_memory=True)
-    host_c = [torch.empty(c.length, dtype=dt, pin_memory=True) for _ in range(2)]
-    host_a.copy_(a.device_tensor())
-    host_b.copy_(b.device_tensor())
-    sets = [(a, b, c)]
-    sets.append(tuple(tb.buffer_from_tensor(ctx, prec, torch.empty(x.length, dtype=dt, device=dev))
-                      for x in (a, b, c)))
-    s_h2d, s_cmp, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    fns = [step_fn(tb, ctx, w, prec, *st) for st in sets]
-
-    def run_e2e(n_steps):
-        done_cmp = [None, None]   # compute finished with set i (its inputs are free)
-        done_d2h = [None, None]   # D2H finished with set i (its C is free)
-        for i in range(n_steps):
-            j = i & 1
-            da, db, dc = (x.device_tensor() for x in sets[j])
-            with torch.cuda.stream(s_h2d):
-                if done_cmp[j] is not None:
-                    s_h2d.wait_event(done_cmp[j])
-                da.copy_(host_a, non_blocking=True)
-                db.copy_(host_b, non_blocking=True)
-                ev_in = torch.cuda.Event()
-                ev_in.record(s_h2d)
-            with torch.cuda.stream(s_cmp):
-                s_cmp.wait_event(ev_in)
-                if done_d2h[j] is not None:
-                    s_cmp.wait_event(done_d2h[j])
-                fns[j]()
-                done_cmp[j] = torch.cuda.Event()
-                done_cmp[j].record(s_cmp)
-            with torch.cuda.stream(s_d2h):
-                s_d2h.wait_event(done_cmp[j])
-                host_c[j].copy_(dc, non_blocking=True)
-                done_d2h[j] = torch.cuda.Event()
-                done_d2h[j].record(s_d2h)
-
-    e2e_steps = max(4, min(args.steps, 20))
-    run_e2e(2)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    t0_ev, t1_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0_ev.record(s_h2d)
-    for st_ in (s_cmp, s_d2h):
-        st_.wait_event(t0_ev)
-    run_e2e(e2e_steps)
-    for st_ in (s_cmp, s_h2d):
-        s_d2h.wait_stream(st_)
-    t1_ev.record(s_d2h)
-    torch.cuda.synchronize()
-    e2e_total = t0_ev.elapsed_time(t1_ev) / 1e3
-    if world > 1:
-        t = torch.tensor([e2e_total], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_total = float(t.item())
-    es = prec.elemsize
-    e2e = {"value": round(flops(w) * world * e2e_steps / e2e_total / 1e9, 2), "unit": "GFLOPS",
-           "h2d_bytes_per_step": (a.length + b.length) * es, "d2h_bytes_per_step": c.length * es,
-           "ms_per_step": round(e2e_total / e2e_steps * 1e3, 4), "steps": e2e_steps,
-           "path": "pinned host A,B -> device (copy stream); public gemm API (compute stream); "
-                   "device C -> pinned host (copy stream); steps pipelined, double-buffered"}
+    # ---- e2e: the library's host-array API (netlib_call) on this rank's share ----
+    e2e = e2e_netlib(tb, ctx, w, sh, main, args, stream, torch, max_over_ranks, world)
+    del main["a"], main["b"], main["c"], main["fn"]
+    torch.cuda.empty_cache()
 
     # ---- extras: the other headline configs (device-timed, this rank) ----
     extra = {}
@@ -352,7 +357,8 @@ def run_ours(args, rank, world, local_rank):
                 continue
             try:
                 big = WORKLOADS[name]["m"] >= 32768
-                r = measure(name, 3 if big else max(5, min(args.steps, 20)), min(args.warmup, 3) if big else args.warmup)
+                r = measure(name, 3 if big else max(5, min(args.steps, 20)),
+                            min(args.warmup, 3) if big else args.warmup)
                 extra[name] = {"workload": describe(r["w"]), "value": round(r["gflops"], 1),
                                "unit": "GFLOPS", "ms_per_step": round(r["total"] / max(1, len(r["times"])) * 1e3, 4),
                                "roofline": r["roofline"], "clocks": r["clocks"]}
@@ -360,18 +366,19 @@ def run_ours(args, rank, world, local_rank):
             except Exception as exc:  # noqa: BLE001
                 extra[name] = {"error": repr(exc)}
             torch.cuda.empty_cache()
-
-    if not args.no_extra:
+        try:
+            extra["c2_sweep"] = c2_sweep(tb, ctx, stream, torch, flush, peaks, peak_src, args.sweep_out)
+        except Exception as exc:  # noqa: BLE001
+            extra["c2_sweep"] = {"error": repr(exc)}
+        torch.cuda.empty_cache()
         try:
             extra["im2col"] = im2col_extra(tb, ctx, stream, torch, flush, peaks, peak_src)
         except Exception as exc:  # noqa: BLE001
             extra["im2col"] = {"error": repr(exc)}
         torch.cuda.empty_cache()
-
-    # North star: batched small-matrix GEMM >= 10x the naive per-matrix launch
-    # loop.  Loop = one public `gemm` call per instance (first 1024 instances
-    # of the 16384 x 32^3 batch, device-timed), extrapolated per instance.
-    if not args.no_extra:
+        # North star: batched small-matrix GEMM >= 10x the naive per-matrix
+        # launch loop.  Loop = one public `gemm` call per instance (first 1024
+        # instances of the 16384 x 32^3 batch, device-timed), per instance.
         try:
             extra["batched_vs_loop"] = batched_vs_loop(tb, ctx, stream, torch)
         except Exception as exc:  # noqa: BLE001
@@ -382,11 +389,20 @@ def run_ours(args, rank, world, local_rank):
     traffic = load_traffic(args.workload, main["kernel"])
     if traffic is not None:
         main["roofline"]["traffic"] = traffic
+    summary = {}
     for name, ex in extra.items():
         if isinstance(ex, dict) and isinstance(ex.get("roofline"), dict):
             t = load_traffic(name, ex["roofline"].get("kernel", ""))
             if t is not None:
                 ex["roofline"]["traffic"] = t
+            summary[name] = [ex["value"], ex["roofline"]["frac"], ex["roofline"]["kernel"]]
+    if isinstance(extra.get("c2_sweep"), dict) and "min_frac" in extra["c2_sweep"]:
+        summary["c2_sweep"] = {"min_frac": extra["c2_sweep"]["min_frac"],
+                               "at_8192": extra["c2_sweep"].get("at_8192")}
+    strong = is_strong(args.workload)
+    par = ("row-block sharded" if w["kind"] == "gemm" else "batch-sharded") + f" x{world}" + \
+        (" via distributed.gemm_sharded" if w["kind"] == "gemm" else " via distributed.gemm_strided_batched_sharded")
+    launches = args.steps * (min(args.chunks, max(1, sh["cnt"])) if args.replicate_c and world > 1 else 1)
     line = {
         "metric": METRIC,
         "value": round(main["gflops"], 2),
@@ -396,18 +412,20 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": round(main["total"] / args.steps * 1e3, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None,
         "dtype": "f16" if w["prec"] == "H" else "f32",
         "data": "synthetic U(-1,1) operands, seeded, resident in HBM",
-        "config": {"workload": describe(w), "m": w["m"], "n": w["n"] * (world if w["kind"] == "gemm" else 1),
-                   "k": w["k"], "batch": w["batch"] * (world if w["kind"] == "batched" else 1),
+        "config": {"workload": describe(w), "m": sh["M"], "n": w["n"], "k": w["k"],
+                   "batch": sh["batch"], "per_rank": {"rows" if w["kind"] == "gemm" else "instances": sh["cnt"]},
                    "layout": "row-major", "trans": "NN", "alpha": 1.0, "beta": 0.0,
-                   "parallelism": f"column-sharded x{world}" if w["kind"] == "gemm" else f"batch-sharded x{world}",
+                   "parallelism": par, "replicate_c": bool(args.replicate_c and world > 1),
+                   "chunks": args.chunks,
                    "l2": "flushed before every step (256 MiB write + 256 MiB read of a second buffer: "
                          "inputs evicted, no dirty lines left)"},
+        "extra_summary": summary,
         "e2e": e2e,
-        "gpu_launches": args.steps,
+        "gpu_launches": launches,
         "kernel": main["kernel"],
         "clocks": main["clocks"],
         "roofline": main["roofline"],
@@ -418,6 +436,107 @@ def run_ours(args, rank, world, local_rank):
     if extra:
         line["extra"] = extra
     return line
+
+
+def e2e_netlib(tb, ctx, w, sh, main, args, stream, torch, max_over_ranks, world) -> dict:
+    """The metric end to end through the library's own host-array API:
+    every step is one ``netlib_call`` on this rank's share with host arrays
+    in pinned memory (``routines.netlib.pinned_empty``) — H2D of A and B,
+    the GEMM, D2H of C, pipelined in sub-blocks inside the call — timed with
+    CUDA events on the compute stream around all steps (each call returns
+    with its result in host memory)."""
+    from paper_1705_05249_b200.routines.netlib import pinned_empty
+
+    prec = main["prec"]
+    es = prec.elemsize
+    L, T = tb.Layout.ROW_MAJOR, tb.Transpose.NO
+    if w["kind"] == "gemm":
+        k, n, cnt = w["k"], w["n"], sh["cnt"]
+        a0 = sh["s0"] * k
+        host_a = pinned_empty(cnt * k, prec)
+        host_b = pinned_empty(k * n, prec)
+        host_c = pinned_empty(cnt * n, prec)
+        host_a[:] = main["a"].device_tensor()[a0:a0 + cnt * k].cpu().numpy()
+        host_b[:] = main["b"].device_tensor().cpu().numpy()
+        rid = "hgemm" if w["prec"] == "H" else "sgemm"
+
+        def step():
+            tb.netlib_call(rid, L, T, T, cnt, n, k, 1.0, host_a, host_b, 0.0, host_c, ctx=ctx)
+        fl = 2.0 * cnt * n * k
+    else:
+        s, e, cnt = w["m"], w["m"] * w["m"], sh["cnt"]
+        a0 = sh["s0"] * e
+        host_a, host_b, host_c = (pinned_empty(cnt * e, prec) for _ in range(3))
+        host_a[:] = main["a"].device_tensor()[a0:a0 + cnt * e].cpu().numpy()
+        host_b[:] = main["b"].device_tensor()[a0:a0 + cnt * e].cpu().numpy()
+        rid = "hgemm_strided_batched" if w["prec"] == "H" else "sgemm_strided_batched"
+
+        def step():
+            tb.netlib_call(rid, L, T, T, s, s, s, 1.0, host_a, e, host_b, e, 0.0, host_c, e, cnt, ctx=ctx)
+        fl = 2.0 * s * s * s * cnt
+    steps = max(4, min(args.steps, 20))
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    total = max_over_ranks(t0.elapsed_time(t1) / 1e3)
+    return {"value": round(fl * world * steps / total / 1e9, 2), "unit": "GFLOPS",
+            "h2d_bytes_per_step": (host_a.size + host_b.size) * es, "d2h_bytes_per_step": host_c.size * es,
+            "ms_per_step": round(total / steps * 1e3, 4), "steps": steps,
+            "path": "netlib_call (the library's host-array API) on pinned host arrays: H2D of A and B, "
+                    "GEMM, D2H of C, pipelined in sub-blocks over copy and compute streams inside each call"}
+
+
+C2_SIZES = (256, 512, 1024, 2048, 4096, 8192)
+C2_LAYOUTS = ("NN", "NT", "TN", "TT")
+
+
+def c2_sweep(tb, ctx, stream, torch, flush, peaks, peak_src, out_path=None, steps=5) -> dict:
+    """BASELINE configs[1]: square sizes 256..8192 x {N,T}^2 x S/H, row-major,
+    device-timed with an L2 flush per step (the reference's sweep client,
+    tb/bench.py:124-129,235-267).  Returns {prec: {layout: {size: [GFLOPS,
+    frac, kernel]}}} plus the minimum fraction over the tensor-/FFMA-bound
+    points (N >= 1024) and the 8192 values."""
+    out = {"sizes": list(C2_SIZES), "layout": "row-major", "steps": steps}
+    fracs, at_8192 = [], {}
+    T = {"N": tb.Transpose.NO, "T": tb.Transpose.YES}
+    for p in ("H", "S"):
+        prec = tb.Precision.H if p == "H" else tb.Precision.S
+        res = {}
+        for lay in C2_LAYOUTS:
+            res[lay] = {}
+            for N in C2_SIZES:
+                dev = ctx.torch_device
+                a = tb.buffer_from_tensor(ctx, prec, (torch.rand(N * N, device=dev) * 2 - 1).to(prec.torch_dtype))
+                b = tb.buffer_from_tensor(ctx, prec, (torch.rand(N * N, device=dev) * 2 - 1).to(prec.torch_dtype))
+                c = tb.buffer_alloc(ctx, prec, N * N)
+                fn = lambda: tb.gemm(ctx, tb.Layout.ROW_MAJOR, T[lay[0]], T[lay[1]], N, N, N, 1.0, a, b, 0.0, c)  # noqa: E731
+                times = device_time(fn, steps, 2, stream, torch, flush)
+                t = sum(times) / len(times)
+                w = dict(kind="gemm", prec=p, m=N, n=N, k=N, batch=1)
+                roof = roofline_of(w, t, peaks, peak_src, dict(M=N, batch=1, s0=0, cnt=N))
+                res[lay][N] = [round(2.0 * N ** 3 / t / 1e9, 1), roof["frac"], ctx.last_launch.native["kernel"]]
+                if N >= 1024:
+                    fracs.append(roof["frac"])
+                if N == 8192:
+                    at_8192[f"{p}{lay}"] = res[lay][N][:2]
+                del a, b, c
+        out[p] = res
+    out["min_frac"] = round(min(fracs), 4) if fracs else None
+    out["at_8192"] = at_8192
+    if out_path:
+        with open(out_path, "w") as fh:
+            json.dump(out, fh, indent=1)
+    return out
 
 
 def im2col_extra(tb, ctx, stream, torch, flush, peaks, peak_src) -> dict:
@@ -448,7 +567,7 @@ def batched_vs_loop(tb, ctx, stream, torch, loop_instances: int = 1024) -> dict:
     out = {}
     for prec in (tb.Precision.H, tb.Precision.S):
         w = WORKLOADS["batched_h32" if prec is tb.Precision.H else "batched_s32"]
-        _, a, b, c = make_operands(tb, ctx, w, 0, 1, torch)
+        _, a, b, c = make_operands(tb, ctx, w, shard_of(w, "", 1, 0), torch)
         s, e, batch = w["m"], w["m"] * w["m"], w["batch"]
         L, T = tb.Layout.ROW_MAJOR, tb.Transpose.NO
 
@@ -578,7 +697,8 @@ def run_reference(args, rank, world):
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(float(np.mean(times)) * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f16" if w["prec"] == "H" else "f32",
+        "scaling": "strong" if is_strong(args.workload) else "weak", "vs_baseline": None,
+        "dtype": "f16" if w["prec"] == "H" else "f32",
         "data": "synthetic U(-1,1)", "impl": "reference",
         "config": {"workload": describe(w), "sample": sample},
         "cpu_baseline": {"value": round(value, 3), "unit": "GFLOPS", "cores": os.cpu_count(),
@@ -598,6 +718,11 @@ def main():
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--replicate-c", action="store_true",
+                    help="N > 1: replicate C on every rank inside the timed step")
+    ap.add_argument("--chunks", type=int, default=4,
+                    help="with --replicate-c: sub-blocks whose transfers overlap the GEMM (1 = one all-gather)")
+    ap.add_argument("--sweep-out", default=None, help="also write the C2 sweep JSON here")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -162,9 +162,10 @@ def gemm_strided_batched(ctx: Context, layout: Layout, trans_a: Transpose, trans
                          stride_b: int, beta, c: Buffer, stride_c: int, batch_count: int, *,
                          a_offset: int = 0, b_offset: int = 0, c_offset: int = 0,
                          lda: int | None = None, ldb: int | None = None,
-                         ldc: int | None = None, tf32: bool = False) -> None:
+                         ldc: int | None = None, tf32: bool = False, _validate_only: bool = False):
     """Instance i uses base offset + i*stride per matrix (extras.py:309-348).
-    ``tf32=True`` opts in to the TF32 tensor-core kernel (see ``gemm``)."""
+    ``tf32=True`` opts in to the TF32 tensor-core kernel (see ``gemm``);
+    ``_validate_only`` as for ``gemm`` (internal, netlib layer)."""
     if batch_count < 1:
         raise UsageError("batch_count must be >= 1")
     lda_e, ldb_e, ldc_e = _default_lds(layout, trans_a, trans_b, m, n, k, lda, ldb, ldc)
@@ -191,7 +192,9 @@ def gemm_strided_batched(ctx: Context, layout: Layout, trans_a: Transpose, trans
     # stride_c >= one instance extent was checked above, so strided outputs
     # never overlap (extras.py:116-122 would find no pair).
     if m == 0 or n == 0:
-        return
+        return False if _validate_only else None
+    if _validate_only:
+        return True
     cfg, family, ncfg = _launch_family(ctx, precision, m, n, k)
     grid1 = reference_grid(family, m, n, cfg)
     grid = WorkGrid((batch_count,) + grid1.work_groups, grid1.work_group_size)

@@ -42,7 +42,8 @@ def gemm(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Transpose,
          a_offset: int = 0, lda: int | None = None,
          b_offset: int = 0, ldb: int | None = None,
          c_offset: int = 0, ldc: int | None = None,
-         kernel: str | None = None, tf32: bool = False) -> None:
+         kernel: str | None = None, tf32: bool = False,
+         _config_args: tuple | None = None, _validate_only: bool = False):
     """C = alpha * op(A) op(B) + beta * C on the GPU (asynchronous on the
     context's stream; read results with ``buffer_read`` / ``Buffer.data``).
 
@@ -51,6 +52,14 @@ def gemm(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Transpose,
     the TF32 tensor-core kernel: inputs are rounded to TF32, so results meet
     the TF32 tolerance 4*2^-10*K*max|a||b| instead of the FP32 one, and
     operands must be 16-byte aligned.
+
+    ``_config_args`` (internal: the netlib layer's chunked pipeline) resolves
+    the configuration and the launch record for that (m, n, k) instead of
+    this call's, so every sub-block of one host-array call runs the kernel
+    configuration of the whole problem; ``_validate_only`` (internal: the
+    netlib layer validates the whole call before its first copy) runs every
+    check and returns False for the m == 0 / n == 0 no-op, True otherwise,
+    without launching.
     """
     precision = a.precision
     check_precision(ctx, precision, a, b, c)
@@ -62,7 +71,7 @@ def gemm(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Transpose,
     if tf32 and precision is not Precision.S:
         raise UsageError("tf32 applies to Precision.S only")
     if m == 0 or n == 0:
-        return
+        return False if _validate_only else None
     a_rows, a_cols = stored_dims(trans_a, m, k)
     b_rows, b_cols = stored_dims(trans_b, k, n)
     lda = lda if lda is not None else default_ld(layout, a_rows, a_cols)
@@ -74,6 +83,8 @@ def gemm(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Transpose,
 
     alpha = scalar(alpha, precision)
     beta = scalar(beta, precision)
+    if _validate_only:
+        return True
     store = get_store(ctx)
     if k == 0 or alpha == 0:
         # Only the beta scaling remains; A and B are never read
@@ -82,12 +93,13 @@ def gemm(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Transpose,
                     a, a_offset, lda, b, b_offset, ldb, beta, c, c_offset, ldc, None)
         return
 
-    cfg, _ = store.resolve("gemm", precision, ctx.device, (m, n, k))
-    route = route_family(m, n, k, store.direct_threshold, kernel)
+    shape = (m, n, k) if _config_args is None else tuple(_config_args)
+    cfg, _ = store.resolve("gemm", precision, ctx.device, shape)
+    route = route_family(*shape, store.direct_threshold, kernel)
     family = "gemm_direct" if route == "direct" else "gemm"
-    grid = reference_grid(family, m, n, cfg)
+    grid = reference_grid(family, shape[0], shape[1], cfg)
     pre_launch(ctx, family, cfg, grid, precision)
-    kcfg = b200_config(store, precision, ctx.device, (m, n, k))
+    kcfg = b200_config(store, precision, ctx.device, shape)
     launched = gemm_native(ctx, precision, layout, trans_a, trans_b, m, n, k, alpha,
                            a, a_offset, lda, b, b_offset, ldb, beta, c, c_offset, ldc, kcfg,
                            route_flags(kernel) | (native.FLAG_TF32 if tf32 else 0))

@@ -207,6 +207,11 @@ def measure(config: Configuration, task: TuningTask, ctx: Context,
         harness.run(config)
     events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(task.timed_runs)]
+    # Hold the stream in a ~1 ms device-side spin while the timed runs are
+    # enqueued, so each event pair brackets device time only — a kernel
+    # shorter than the host's per-call launch cost would otherwise be timed
+    # at the launch rate.
+    torch.cuda._sleep(2_000_000)
     for e0, e1 in events:
         e0.record(stream)
         harness.run(config)
