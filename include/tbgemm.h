@@ -160,6 +160,27 @@ int tb_im2col(int prec, int64_t channels, int64_t height, int64_t width,
               int64_t col_off, void* stream);
 
 /*
+ * Implicit GEMM: convolution as im2col + GEMM without materialising the
+ * column matrix (the composition the reference's im2col
+ * exists for, extras.py:56-109: "a weights-as-rows GEMM against it equals
+ * direct cross-correlation").  For each of `batch` images (channel-major,
+ * instance b at im + im_off + b*channels*height*width):
+ *   result[b][f][q] = sum_r kernel[f][r] * col_b[r][q]
+ * with col_b the reference's im2col matrix (r = (ch*kernel_h + ky)*kernel_w +
+ * kx, q = oy*out_w + ox), `kernel` num_kernels x (channels*kernel_h*kernel_w)
+ * row-major from kernel_off, `result` batch x num_kernels x (out_h*out_w)
+ * from result_off (NCHW).  H: FP16 in/out, FP32 accumulation on tcgen05;
+ * S: the FP32 sequential-k chain (bitwise im2col + gemm).  Device pointers.
+ */
+int tb_convgemm(int prec, int64_t channels, int64_t height, int64_t width,
+                int64_t kernel_h, int64_t kernel_w, int64_t pad_h, int64_t pad_w,
+                int64_t stride_h, int64_t stride_w, int64_t dilation_h,
+                int64_t dilation_w, int64_t num_kernels, int64_t batch,
+                const void* im, int64_t im_off, const void* kernel,
+                int64_t kernel_off, void* result, int64_t result_off, int flags,
+                void* stream);
+
+/*
  * Structured level-3 helpers — the reference's transform kinds
  * (kernels/transforms.py:21-147) used by symm/syrk/syr2k/trmm/trsm
  * (routines/level3.py:152-537).  Column-major storage, element offsets.

@@ -35,6 +35,18 @@ struct Problem {
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
+// Implicit-GEMM (convgemm) geometry: op(A)(q, r) of the canonical problem is
+// the im2col matrix entry col[r][q] (reference extras.py:56-109) gathered
+// from the channel-major image of instance z at p.a + off_a(z):
+//   r = (ch*kh + ky)*kw + kx,  q = oy*out_w + ox,
+//   y = oy*stride_h + ky*dil_h - pad_h,  x = ox*stride_w + kx*dil_w - pad_w,
+//   value = image[ch][y][x] inside the image, 0 in the padding.
+struct ConvGeom {
+  int channels, height, width, kh, kw;
+  int pad_h, pad_w, stride_h, stride_w, dil_h, dil_w;
+  int out_h, out_w;
+};
+
 __device__ __forceinline__ int64_t inst_off(int64_t base, int64_t stride,
                                             const int64_t* offs, int64_t z) {
   return offs ? __ldg(offs + z) : base + z * stride;

@@ -31,23 +31,25 @@ bool tma_ok(const Call& c) {
   return hgemm_aligned(c) && !generic && fits && !(c.flags & TB_FLAG_NO_TMA);
 }
 
-template <int BN, bool TMA, bool AMN, bool BMN, bool VEC, int ST = 0>
+template <int BN, bool TMA, bool AMN, bool BMN, bool VEC, int ST = 0, bool CONV = false>
 int launch_hg(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
   using Cfg = HgCfg<BN, TMA, ST>;
   const Problem& p = c.p;
   const int tiles_m = static_cast<int>((p.m + HG_BM - 1) / HG_BM);
   const int tiles_n = static_cast<int>((p.n + BN - 1) / BN);
   const int64_t total = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
-  auto kern = hgemm_tc_kernel<BN, TMA, AMN, BMN, VEC, ST>;
+  auto kern = hgemm_tc_kernel<BN, TMA, AMN, BMN, VEC, ST, CONV>;
   static SmemAttr attr;  // per instantiation, per device
   if (int rc = ensure_smem(attr, kern, Cfg::SMEM_BYTES)) return rc;
   const int sms = sms_or_default();
   const int64_t g = total < sms ? total : sms;
   dim3 grid(static_cast<unsigned>(g)), block(Cfg::THREADS);
-  kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, cfg_group_m(c, 16), total);
+  const ConvGeom geom = c.conv ? *c.conv : ConvGeom{};
+  kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, cfg_group_m(c, 16), total, geom);
   char name[64];
-  snprintf(name, sizeof(name), "hgemm_tc_%s_128x%d_%c%c%s%s", TMA ? "tma" : "ldg", BN, AMN ? 'm' : 'k',
-           BMN ? 'n' : 'k', (!TMA && !VEC) ? "_scalar" : "", ST > 0 ? (ST == 3 ? "_st3" : "_st4") : "");
+  snprintf(name, sizeof(name), "hgemm_tc_%s_128x%d_%c%c%s%s", CONV ? "conv" : (TMA ? "tma" : "ldg"), BN,
+           AMN ? 'm' : 'k', BMN ? 'n' : 'k', (!TMA && !VEC) ? "_scalar" : "",
+           ST > 0 ? (ST == 3 ? "_st3" : "_st4") : "");
   record(name, grid, block, 1, Cfg::SMEM_BYTES, total);
   return check_launch("hgemm_tc launch");
 }
@@ -254,6 +256,28 @@ int dispatch_hsplit(const Call& c, int ks) {
 }
 
 }  // namespace
+
+// Implicit GEMM (tb_convgemm): op(A) gathered from the image by the LDG
+// producer warps (conv_fill_tile), op(B) = the filters (K-contiguous rows),
+// UMMA N narrowed while the tiles leave SMs idle, as for a GEMM.
+int dispatch_hconv(const Call& c) {
+  const Problem& p = c.p;
+  CUtensorMap none;
+  memset(&none, 0, sizeof(none));
+  const bool vec = (p.ldb % 8 == 0) && aligned_elems(p.b, p.b_off, 2, 16);
+  auto tiles = [&](int b) { return ((p.m + HG_BM - 1) / HG_BM) * ((p.n + b - 1) / b) * p.batch; };
+  const int sms = sms_or_default();
+  int bn = 256;
+  while (bn > 64 && tiles(bn) < sms) bn /= 2;
+  if (vec) {
+    if (bn == 256) return launch_hg<256, false, true, false, true, 0, true>(c, none, none);
+    if (bn == 128) return launch_hg<128, false, true, false, true, 0, true>(c, none, none);
+    return launch_hg<64, false, true, false, true, 0, true>(c, none, none);
+  }
+  if (bn == 256) return launch_hg<256, false, true, false, false, 0, true>(c, none, none);
+  if (bn == 128) return launch_hg<128, false, true, false, false, 0, true>(c, none, none);
+  return launch_hg<64, false, true, false, false, 0, true>(c, none, none);
+}
 
 int dispatch_hgemm(const Call& c) {
   // Small instances (m, n <= 64): packed tcgen05 kernel.  Bitwise identical to

@@ -120,6 +120,68 @@ __device__ __forceinline__ void ldg_fill_tile(uint8_t* smem, const __half* base,
 }
 
 
+// Implicit-GEMM producer for op(A) (128 positions x 64 K, MN-major layout of
+// ldg_fill_tile): every element is gathered from the image (ConvGeom), zero
+// in the padding and past m / k.  Each thread owns the same 16 positions of a
+// tile (two groups of 8 at c*8 and 64 + c*8, c = tid % 8) and K rows
+// tid/8 + 16*i; `yb`/`xb` hold oy*stride - pad / ox*stride - pad per owned
+// position (INT_MIN/2 for positions past m), computed once per tile.
+__device__ __forceinline__ void conv_tile_coords(const ConvGeom& g, int64_t m, int64_t m0, int tid,
+                                                 int (&yb)[16], int (&xb)[16]) {
+  const int c = tid & 7;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int64_t q = m0 + (i >> 3) * 64 + c * 8 + (i & 7);
+    if (q < m) {
+      const int oy = static_cast<int>(q / g.out_w), ox = static_cast<int>(q - static_cast<int64_t>(oy) * g.out_w);
+      yb[i] = oy * g.stride_h - g.pad_h;
+      xb[i] = ox * g.stride_w - g.pad_w;
+    } else {
+      yb[i] = -(1 << 30);
+      xb[i] = -(1 << 30);
+    }
+  }
+}
+
+__device__ __forceinline__ void conv_fill_tile(uint8_t* smem, const __half* im, const ConvGeom& g,
+                                               int64_t k0, int k_left, int tid, const int (&yb)[16],
+                                               const int (&xb)[16]) {
+  const uint16_t* im16 = reinterpret_cast<const uint16_t*>(im);
+  const int khw = g.kh * g.kw;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = (tid >> 3) + 16 * i;                 // K row of this K block
+    uint16_t h[16];
+    if (r < k_left) {
+      const int kr = static_cast<int>(k0) + r;
+      const int ch = kr / khw, rem = kr - ch * khw;
+      const int ky = rem / g.kw, kx = rem - ky * g.kw;
+      const int dy = ky * g.dil_h, dx = kx * g.dil_w;
+      const uint16_t* plane = im16 + static_cast<int64_t>(ch) * g.height * g.width;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int y = yb[j] + dy, x = xb[j] + dx;
+        h[j] = (static_cast<unsigned>(y) < static_cast<unsigned>(g.height) &&
+                static_cast<unsigned>(x) < static_cast<unsigned>(g.width))
+                   ? __ldg(plane + static_cast<int64_t>(y) * g.width + x)
+                   : static_cast<uint16_t>(0);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) h[j] = 0;
+    }
+#pragma unroll
+    for (int sub = 0; sub < 2; ++sub) {
+      uint4 v;
+      v.x = h[sub * 8 + 0] | (static_cast<uint32_t>(h[sub * 8 + 1]) << 16);
+      v.y = h[sub * 8 + 2] | (static_cast<uint32_t>(h[sub * 8 + 3]) << 16);
+      v.z = h[sub * 8 + 4] | (static_cast<uint32_t>(h[sub * 8 + 5]) << 16);
+      v.w = h[sub * 8 + 6] | (static_cast<uint32_t>(h[sub * 8 + 7]) << 16);
+      *reinterpret_cast<uint4*>(smem + sub * 8192 + sw128_off(r, tid & 7)) = v;
+    }
+  }
+}
+
 // K16 MMA steps in K block kb: 4, except in the last block, where steps that
 // would multiply only zero padding are not issued.  Every H kernel uses this
 // rule, so all H paths issue the same MMA sequence for an output element.
@@ -231,10 +293,14 @@ __device__ __forceinline__ void epi_store_block(float* stage, const uint32_t (&v
   __syncwarp();
 }
 
-template <int BN, bool TMA, bool A_MN, bool B_MN, bool VEC, int ST = 0>
+// CONV: op(A) is gathered from an image (implicit GEMM, ConvGeom; LDG
+// producer, A_MN layout); otherwise `conv` is unused.
+template <int BN, bool TMA, bool A_MN, bool B_MN, bool VEC, int ST = 0, bool CONV = false>
 __global__ void __launch_bounds__(HgCfg<BN, TMA, ST>::THREADS, 1)
     hgemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    Problem p, int tiles_m, int tiles_n, int group_m, int64_t total_tiles) {
+                    Problem p, int tiles_m, int tiles_n, int group_m, int64_t total_tiles,
+                    const ConvGeom conv) {
+  static_assert(!CONV || (!TMA && A_MN), "the im2col gather runs in the LDG producer, MN-major");
   using C = HgCfg<BN, TMA, ST>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -318,6 +384,8 @@ __global__ void __launch_bounds__(HgCfg<BN, TMA, ST>::THREADS, 1)
         const __half* B = static_cast<const __half*>(p.b) + inst_off(p.b_off, p.stride_b, p.b_offs, z);
         const int m_left = static_cast<int>(min64(HG_BM, p.m - m0));
         const int n_left = static_cast<int>(min64(BN, p.n - n0));
+        int yb[16], xb[16];
+        if (CONV) conv_tile_coords(conv, p.m, m0, tid, yb, xb);
         for (int kb = 0; kb < nkb; ++kb) {
           const int64_t k0 = static_cast<int64_t>(kb) * HG_BK;
           const int k_left = static_cast<int>(min64(HG_BK, p.k - k0));
@@ -325,7 +393,10 @@ __global__ void __launch_bounds__(HgCfg<BN, TMA, ST>::THREADS, 1)
           // A: K-major element (i,kk) at A[i*lda + kk]; MN-major at A[i + kk*lda]
           const __half* a_base = A_MN ? A + k0 * p.lda + m0 : A + m0 * p.lda + k0;
           const __half* b_base = B_MN ? B + k0 * p.ldb + n0 : B + n0 * p.ldb + k0;
-          ldg_fill_tile<HG_BM, A_MN, VEC>(sA + s * C::A_BYTES, a_base, p.lda, m_left, k_left, tid);
+          if (CONV)
+            conv_fill_tile(sA + s * C::A_BYTES, A, conv, k0, k_left, tid, yb, xb);
+          else
+            ldg_fill_tile<HG_BM, A_MN, VEC>(sA + s * C::A_BYTES, a_base, p.lda, m_left, k_left, tid);
           ldg_fill_tile<BN, B_MN, VEC>(sB + s * C::B_BYTES, b_base, p.ldb, n_left, k_left, tid);
           fence_proxy_async_smem();
           mbar_arrive(&full[s]);

@@ -24,6 +24,7 @@ struct Call {
   Problem p;
   int offs_aligned;            // generic batched: host-asserted offset alignment
   const tb_gemm_config* cfg;   // NULL: shape routing (built-in)
+  const ConvGeom* conv;        // tb_convgemm: op(A) gathered from an image
   int flags;
   cudaStream_t stream;
 };
@@ -85,6 +86,8 @@ int dispatch_sgemm_tma(const Call& c, int tile, int mwg, int nwg);   // sgemm_tm
 int dispatch_hgemm(const Call& c);                                   // hgemm.cu
 int dispatch_hsmall_any(const Call& c);                              // hgemm_small.cu
 int launch_hscale(const Call& c);                                    // hgemm.cu
+int dispatch_hconv(const Call& c);                                   // hgemm.cu
+int dispatch_sconv(const Call& c);                                   // sgemm.cu
 
 }  // namespace host
 }  // namespace tb

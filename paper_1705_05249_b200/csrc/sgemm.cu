@@ -13,7 +13,7 @@ namespace tb {
 namespace host {
 namespace {
 
-template <int BM, int BN, int BK, int TM, int TN, bool VEC, int MINB>
+template <int BM, int BN, int BK, int TM, int TN, bool VEC, int MINB, bool CONV = false>
 int launch_simt(const Call& c) {
   const Problem& p = c.p;
   const int tiles_m = static_cast<int>((p.m + BM - 1) / BM);
@@ -23,15 +23,22 @@ int launch_simt(const Call& c) {
   const int group_m = cfg_group_m(c, 8);
   dim3 grid(static_cast<unsigned>(blocks)), block(SimtShape<BM, BN, BK, TM, TN>::NT);
   const int sel = (p.a_kcontig ? 2 : 0) | (p.b_ncontig ? 1 : 0);
-  switch (sel) {
-    case 0: sgemm_simt_kernel<BM, BN, BK, TM, TN, false, false, VEC, MINB><<<grid, block, 0, c.stream>>>(p, tiles_m, tiles_n, group_m); break;
-    case 1: sgemm_simt_kernel<BM, BN, BK, TM, TN, false, true, VEC, MINB><<<grid, block, 0, c.stream>>>(p, tiles_m, tiles_n, group_m); break;
-    case 2: sgemm_simt_kernel<BM, BN, BK, TM, TN, true, false, VEC, MINB><<<grid, block, 0, c.stream>>>(p, tiles_m, tiles_n, group_m); break;
-    default: sgemm_simt_kernel<BM, BN, BK, TM, TN, true, true, VEC, MINB><<<grid, block, 0, c.stream>>>(p, tiles_m, tiles_n, group_m); break;
+  const ConvGeom geom = c.conv ? *c.conv : ConvGeom{};
+  if constexpr (CONV) {  // op(A) gathered (M-contiguous layout), filters K-contiguous
+    sgemm_simt_kernel<BM, BN, BK, TM, TN, false, false, VEC, MINB, true><<<grid, block, 0, c.stream>>>(
+        p, tiles_m, tiles_n, group_m, geom);
+  } else {
+    switch (sel) {
+      case 0: sgemm_simt_kernel<BM, BN, BK, TM, TN, false, false, VEC, MINB><<<grid, block, 0, c.stream>>>(p, tiles_m, tiles_n, group_m, geom); break;
+      case 1: sgemm_simt_kernel<BM, BN, BK, TM, TN, false, true, VEC, MINB><<<grid, block, 0, c.stream>>>(p, tiles_m, tiles_n, group_m, geom); break;
+      case 2: sgemm_simt_kernel<BM, BN, BK, TM, TN, true, false, VEC, MINB><<<grid, block, 0, c.stream>>>(p, tiles_m, tiles_n, group_m, geom); break;
+      default: sgemm_simt_kernel<BM, BN, BK, TM, TN, true, true, VEC, MINB><<<grid, block, 0, c.stream>>>(p, tiles_m, tiles_n, group_m, geom); break;
+    }
   }
   char name[64];
   static const char* lay[4] = {"mk", "mn", "kk", "kn"};  // A major x B major
-  snprintf(name, sizeof(name), "sgemm_simt_%dx%dx%d_%s_%s", BM, BN, BK, VEC ? "vec" : "gen", lay[sel]);
+  snprintf(name, sizeof(name), "sgemm_%s_%dx%dx%d_%s_%s", CONV ? "conv" : "simt", BM, BN, BK,
+           VEC ? "vec" : "gen", lay[sel]);
   record(name, grid, block, 1, 0, blocks);
   return check_launch("sgemm_simt launch");
 }
@@ -152,6 +159,18 @@ int simt_tile(const Call& c, int mwg, int nwg) {
 }
 
 }  // namespace
+
+// Implicit GEMM (tb_convgemm) for S: the register-staged FFMA2 kernel with
+// op(A) gathered from the image (simt_conv_stage).  The gathered values are
+// the im2col entries exactly, so results equal im2col + gemm bitwise (the
+// sequential-k chain).  64x64 tiles (4x4 micro-tiles) keep the SMs busy at
+// the typical layer shapes (a few thousand positions x tens of filters).
+int dispatch_sconv(const Call& c) {
+  const Problem& p = c.p;
+  const bool vec = (p.ldb % 4 == 0) && aligned_elems(p.b, p.b_off, 4, 16);
+  if (vec) return launch_simt<64, 64, 16, 4, 4, true, 2, true>(c);
+  return launch_simt<64, 64, 16, 4, 4, false, 2, true>(c);
+}
 
 int dispatch_sgemm(const Call& c) {
   const Problem& p = c.p;

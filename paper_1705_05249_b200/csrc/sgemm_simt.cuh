@@ -82,6 +82,42 @@ __device__ __forceinline__ void simt_load_stage(float4 (&r)[PER_T], const float*
   }
 }
 
+// Implicit-GEMM variant of simt_load_stage for op(A) (M-contiguous chunk
+// layout): chunk e holds positions q = m0 + row .. +3 of K index k0 + kk,
+// gathered from the channel-major image `im` (ConvGeom; zero in the padding,
+// past m and past k).
+template <int ROWS, int BK, int PER_T, int NT>
+__device__ __forceinline__ void simt_conv_stage(float4 (&r)[PER_T], const float* __restrict__ im,
+                                                const ConvGeom& g, int64_t m, int64_t m0, int64_t k0,
+                                                int k_left) {
+  const int khw = g.kh * g.kw;
+#pragma unroll
+  for (int j = 0; j < PER_T; ++j) {
+    const int e = threadIdx.x + j * NT;
+    const int kk = e / (ROWS / 4);
+    const int row = (e % (ROWS / 4)) * 4;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (kk < k_left) {
+      const int kr = static_cast<int>(k0) + kk;
+      const int ch = kr / khw, rem = kr - ch * khw;
+      const int ky = rem / g.kw, kx = rem - ky * g.kw;
+      const float* plane = im + static_cast<int64_t>(ch) * g.height * g.width;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t pos = m0 + row + q;
+        if (pos < m) {
+          const int oy = static_cast<int>(pos / g.out_w), ox = static_cast<int>(pos - static_cast<int64_t>(oy) * g.out_w);
+          const int y = oy * g.stride_h + ky * g.dil_h - g.pad_h, x = ox * g.stride_w + kx * g.dil_w - g.pad_w;
+          if (static_cast<unsigned>(y) < static_cast<unsigned>(g.height) &&
+              static_cast<unsigned>(x) < static_cast<unsigned>(g.width))
+            v[q] = __ldg(plane + static_cast<int64_t>(y) * g.width + x);
+        }
+      }
+    }
+    r[j] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
 // Store the register stage into shared memory laid out [BK][ROWS+PAD]
 // (contiguous along M or N so the compute loop reads 128-bit fragments).
 template <int ROWS, int BK, bool KCONTIG, int PER_T, int NT, int LDS>
@@ -120,10 +156,12 @@ __device__ __forceinline__ void tile_coords(int64_t bid, int tiles_m, int tiles_
   nt = rr / gm;
 }
 
-template <int BM, int BN, int BK, int TM, int TN, bool AK, bool BNC, bool VEC, int MINB>
+// CONV: op(A) gathered from an image (implicit GEMM, ConvGeom; AK false).
+template <int BM, int BN, int BK, int TM, int TN, bool AK, bool BNC, bool VEC, int MINB, bool CONV = false>
 __global__ void __launch_bounds__(SimtShape<BM, BN, BK, TM, TN>::NT, MINB)
-    sgemm_simt_kernel(Problem p, int tiles_m, int tiles_n, int group_m) {
+    sgemm_simt_kernel(Problem p, int tiles_m, int tiles_n, int group_m, const ConvGeom conv) {
   using S = SimtShape<BM, BN, BK, TM, TN>;
+  static_assert(!CONV || !AK, "the im2col gather fills the M-contiguous layout");
   __shared__ __align__(16) float As[2][BK * S::LDA_S];
   __shared__ __align__(16) float Bs[2][BK * S::LDB_S];
 
@@ -161,7 +199,11 @@ __global__ void __launch_bounds__(SimtShape<BM, BN, BK, TM, TN>::NT, MINB)
     float4 ra[S::A_PER_T], rb[S::B_PER_T];
     int k_left = static_cast<int>(min64(p.k, 0x7fffffff));
 
-    simt_load_stage<BM, BK, AK, VEC, S::A_PER_T, S::NT>(ra, a_tile, p.lda, rows_m, k_left);
+    int64_t kpos = 0;   // K index of the stage being loaded (CONV)
+    if (CONV)
+      simt_conv_stage<BM, BK, S::A_PER_T, S::NT>(ra, A, conv, p.m, m0, 0, k_left);
+    else
+      simt_load_stage<BM, BK, AK, VEC, S::A_PER_T, S::NT>(ra, a_tile, p.lda, rows_m, k_left);
     simt_load_stage<BN, BK, !BNC, VEC, S::B_PER_T, S::NT>(rb, b_tile, p.ldb, cols_n, k_left);
     simt_store_stage<BM, BK, AK, S::A_PER_T, S::NT, S::LDA_S>(As[0], ra);
     simt_store_stage<BN, BK, !BNC, S::B_PER_T, S::NT, S::LDB_S>(Bs[0], rb);
@@ -173,7 +215,11 @@ __global__ void __launch_bounds__(SimtShape<BM, BN, BK, TM, TN>::NT, MINB)
       if (kt + 1 < ktiles) {
         a_tile += a_kstep;
         b_tile += b_kstep;
-        simt_load_stage<BM, BK, AK, VEC, S::A_PER_T, S::NT>(ra, a_tile, p.lda, rows_m, k_left - BK);
+        kpos += BK;
+        if (CONV)
+          simt_conv_stage<BM, BK, S::A_PER_T, S::NT>(ra, A, conv, p.m, m0, kpos, k_left - BK);
+        else
+          simt_load_stage<BM, BK, AK, VEC, S::A_PER_T, S::NT>(ra, a_tile, p.lda, rows_m, k_left - BK);
         simt_load_stage<BN, BK, !BNC, VEC, S::B_PER_T, S::NT>(rb, b_tile, p.ldb, cols_n, k_left - BK);
       }
       const float* as = As[cur];

@@ -271,6 +271,64 @@ int tb_gemm_batched(int prec, int layout, int trans_a, int trans_b, int64_t m, i
   return run(call);
 }
 
+int tb_convgemm(int prec, int64_t channels, int64_t height, int64_t width, int64_t kernel_h, int64_t kernel_w,
+                int64_t pad_h, int64_t pad_w, int64_t stride_h, int64_t stride_w, int64_t dilation_h,
+                int64_t dilation_w, int64_t num_kernels, int64_t batch, const void* im, int64_t im_off,
+                const void* kernel, int64_t kernel_off, void* result, int64_t result_off, int flags,
+                void* stream) {
+  memset(&g_last, 0, sizeof(g_last));
+  const int64_t lim = (1LL << 31) - 1;
+  if (channels < 1 || height < 1 || width < 1 || kernel_h < 1 || kernel_w < 1 || stride_h < 1 || stride_w < 1 ||
+      dilation_h < 1 || dilation_w < 1 || num_kernels < 0 || batch < 1 || !im || !kernel || !result) {
+    snprintf(g_last_err, sizeof(g_last_err), "convgemm: invalid geometry");
+    return TB_ERR_INVALID;
+  }
+  const int64_t span_h = dilation_h * (kernel_h - 1) + 1, span_w = dilation_w * (kernel_w - 1) + 1;
+  const int64_t out_h = (height + 2 * pad_h - span_h) / stride_h + 1;
+  const int64_t out_w = (width + 2 * pad_w - span_w) / stride_w + 1;
+  if (height + 2 * pad_h < span_h || width + 2 * pad_w < span_w || out_h <= 0 || out_w <= 0) {
+    snprintf(g_last_err, sizeof(g_last_err), "convgemm: output dimensions are not positive");
+    return TB_ERR_INVALID;
+  }
+  const int64_t K = channels * kernel_h * kernel_w, N = out_h * out_w;
+  if (channels * height * width > lim || K > lim || N > lim || height > lim || width > lim || pad_h > lim ||
+      pad_w > lim || pad_h < -lim || pad_w < -lim || stride_h > lim || stride_w > lim || dilation_h > lim ||
+      dilation_w > lim || kernel_h * kernel_w > lim) {
+    snprintf(g_last_err, sizeof(g_last_err), "convgemm: geometry exceeds the 32-bit index range of the kernel");
+    return TB_ERR_UNSUPPORTED;
+  }
+  if (num_kernels == 0) return TB_OK;
+  ConvGeom g;
+  g.channels = static_cast<int>(channels); g.height = static_cast<int>(height); g.width = static_cast<int>(width);
+  g.kh = static_cast<int>(kernel_h); g.kw = static_cast<int>(kernel_w);
+  g.pad_h = static_cast<int>(pad_h); g.pad_w = static_cast<int>(pad_w);
+  g.stride_h = static_cast<int>(stride_h); g.stride_w = static_cast<int>(stride_w);
+  g.dil_h = static_cast<int>(dilation_h); g.dil_w = static_cast<int>(dilation_w);
+  g.out_h = static_cast<int>(out_h); g.out_w = static_cast<int>(out_w);
+  // Canonical column-major problem: C'(q, f) = sum_r col[r][q] * kernel[f][r]
+  //   m = N positions, n = num_kernels filters, k = K;
+  //   op(A) gathered (MN-major), B' = kernel rows (K-contiguous, ldb = K),
+  //   C' = result plane per filter (ldc = N) — the NCHW output.
+  Call c;
+  memset(&c, 0, sizeof(c));
+  c.prec = prec;
+  c.m = N; c.n = num_kernels; c.k = K;
+  c.p.m = N; c.p.n = num_kernels; c.p.k = K;
+  c.p.a = im; c.p.a_off = im_off; c.p.stride_a = channels * height * width; c.p.lda = 1;
+  c.p.b = kernel; c.p.b_off = kernel_off; c.p.ldb = K; c.p.stride_b = 0;
+  c.p.c = result; c.p.c_off = result_off; c.p.ldc = N; c.p.stride_c = num_kernels * N;
+  c.p.alpha = 1.0f; c.p.beta = 0.0f;
+  c.p.batch = batch;
+  c.p.a_kcontig = 0; c.p.b_ncontig = 0;
+  c.conv = &g;
+  c.flags = flags;
+  c.stream = static_cast<cudaStream_t>(stream);
+  if (prec == TB_PREC_H) return dispatch_hconv(c);
+  if (prec == TB_PREC_S) return dispatch_sconv(c);
+  snprintf(g_last_err, sizeof(g_last_err), "convgemm: precision must be H or S");
+  return TB_ERR_UNSUPPORTED;
+}
+
 int tb_im2col(int prec, int64_t channels, int64_t height, int64_t width, int64_t kernel_h, int64_t kernel_w,
               int64_t pad_h, int64_t pad_w, int64_t stride_h, int64_t stride_w, int64_t dilation_h,
               int64_t dilation_w, const void* im, int64_t im_off, void* col, int64_t col_off, void* stream) {

@@ -49,6 +49,7 @@ TB_OK = 0
 #: Every symbol include/tbgemm.h declares (checked by tests/test_native_abi.py).
 EXPORTED_SYMBOLS = (
     "tb_gemm",
+    "tb_convgemm",
     "tb_im2col",
     "tb_transform",
     "tb_convert_f32",
@@ -136,6 +137,8 @@ def _declare(so) -> None:
         _i32, _i32, _i32, _i32, _i64, _i64, _i64, _vp,
         _vp, _vp, _i64, _vp, _vp, _i64, _vp,
         _vp, _vp, _i64, _i64, _i32, _P(TbGemmConfig), _i32, _vp]
+    so.tb_convgemm.restype = _i32
+    so.tb_convgemm.argtypes = [_i32] + [_i64] * 13 + [_vp, _i64, _vp, _i64, _vp, _i64, _i32, _vp]
     so.tb_im2col.restype = _i32
     so.tb_im2col.argtypes = [_i32] + [_i64] * 11 + [_vp, _i64, _vp, _i64, _vp]
     so.tb_transform.restype = _i32

@@ -14,10 +14,10 @@ from ..core import Buffer, Context
 from ..errors import UsageError
 from ..kernels import native
 from ..kernels.dispatch import prec_code, require_gpu
-from ..kernels.engine import launch_grid, pre_launch, record_launch
+from ..kernels.engine import WorkGrid, launch_grid, pre_launch, record_launch, reference_grid
 from .common import check_precision, get_store
 
-__all__ = ["im2col", "im2col_geometry"]
+__all__ = ["im2col", "im2col_geometry", "convgemm"]
 
 
 def im2col_geometry(channels, height, width, kernel_h, kernel_w, pad_h, pad_w,
@@ -70,3 +70,57 @@ def im2col(ctx: Context, channels: int, height: int, width: int,
     col.mark_device_written()
     native.check(st, "tb_im2col")
     record_launch(ctx, "transform", cfg, grid, native.last_launch())
+
+
+def convgemm(ctx: Context, channels: int, height: int, width: int,
+             kernel_h: int, kernel_w: int, pad_h: int, pad_w: int,
+             stride_h: int, stride_w: int, dilation_h: int, dilation_w: int,
+             num_kernels: int, batch_count: int, im: Buffer, kernel: Buffer, result: Buffer, *,
+             im_offset: int = 0, kernel_offset: int = 0, result_offset: int = 0) -> None:
+    """Convolution as an implicit GEMM: for each of
+    ``batch_count`` channel-major images,
+
+        result[b][f][q] = sum_r kernel[f][r] * im2col(image_b)[r][q]
+
+    — exactly ``im2col`` (same geometry, checks and column order) followed by
+    the weights-as-rows GEMM its docstring describes (extras.py:56-66), but
+    the column matrix is never materialised: the GEMM's A-operand producer
+    gathers it from the image tile by tile (csrc/hgemm_tc.cuh
+    conv_fill_tile, csrc/sgemm_simt.cuh simt_conv_stage).
+
+    ``kernel`` holds num_kernels rows of channels*kernel_h*kernel_w weights
+    (row-major); image b starts at im_offset + b*channels*height*width and
+    its output plane block at result_offset + b*num_kernels*out_h*out_w
+    (NCHW).  S results equal im2col + gemm bitwise (sequential-k chain); H
+    accumulates in FP32 on the tensor cores and rounds once to FP16.
+    Asynchronous on the context's stream.
+    """
+    precision = im.precision
+    check_precision(ctx, precision, im, kernel, result)
+    out_h, out_w, rows, cols = im2col_geometry(
+        channels, height, width, kernel_h, kernel_w, pad_h, pad_w,
+        stride_h, stride_w, dilation_h, dilation_w)
+    if num_kernels < 0:
+        raise UsageError("num_kernels must be >= 0")
+    if batch_count < 1:
+        raise UsageError("batch_count must be >= 1")
+    im.check_range(im_offset, batch_count * channels * height * width)
+    kernel.check_range(kernel_offset, num_kernels * rows)
+    result.check_range(result_offset, batch_count * num_kernels * cols)
+    pcode = prec_code(precision)
+    if num_kernels == 0:
+        return
+    store = get_store(ctx)
+    cfg, _ = store.resolve("gemm", precision, ctx.device, (cols, num_kernels, rows))
+    grid1 = reference_grid("gemm", cols, num_kernels, cfg)
+    grid = WorkGrid((batch_count,) + grid1.work_groups, grid1.work_group_size)
+    pre_launch(ctx, "gemm", cfg, grid, precision)
+    require_gpu(ctx)
+    so = native.lib()
+    st = so.tb_convgemm(pcode, channels, height, width, kernel_h, kernel_w, pad_h, pad_w,
+                        stride_h, stride_w, dilation_h, dilation_w, num_kernels, batch_count,
+                        im.data_ptr(), im_offset, kernel.data_ptr(), kernel_offset,
+                        result.data_ptr(), result_offset, 0, ctx.stream_handle())
+    result.mark_device_written()
+    native.check(st, "tb_convgemm")
+    record_launch(ctx, "convgemm", cfg, grid, native.last_launch())
