@@ -107,11 +107,13 @@ int dispatch_tf32_bn(const Call& c) {
   memset(&ta, 0, sizeof(ta));
   memset(&tbm, 0, sizeof(tbm));
   const CUtensorMapDataType F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  // MN-major FP32 operands: 32-byte swizzle atoms (sgemm_tf32_tc.cuh)
+  const CUtensorMapSwizzle MN32 = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
   int rc = !amn ? make_map(&ta, A, p.k, p.m, p.batch, p.lda, p.stride_a, 32, 128, F32, 4)
-                : make_map(&ta, A, p.m, p.k, p.batch, p.lda, p.stride_a, 32, 32, F32, 4);
+                : make_map(&ta, A, p.m, p.k, p.batch, p.lda, p.stride_a, 32, 32, F32, 4, MN32);
   if (rc != TB_OK) return rc;
   rc = !bmn ? make_map(&tbm, B, p.k, p.n, p.batch, p.ldb, p.stride_b, 32, BN, F32, 4)
-            : make_map(&tbm, B, p.n, p.k, p.batch, p.ldb, p.stride_b, 32, 32, F32, 4);
+            : make_map(&tbm, B, p.n, p.k, p.batch, p.ldb, p.stride_b, 32, 32, F32, 4, MN32);
   if (rc != TB_OK) return rc;
   if (!amn && !bmn) return launch_tf32<BN, false, false>(c, ta, tbm);
   if (!amn && bmn) return launch_tf32<BN, false, true>(c, ta, tbm);
@@ -129,14 +131,6 @@ int dispatch_tf32(const Call& c) {
   if (!ok) {
     snprintf(err_buf(), 256,
              "TF32 path needs 16-byte aligned operands (ld and offsets multiples of 4) and strided batches");
-    return TB_ERR_UNSUPPORTED;
-  }
-  // UMMA reads MN-major 32-bit operands only in the SWIZZLE_128B_BASE32B
-  // canonical layout, which this version does not build: K-major operands
-  // only (col-major T x N, row-major N x T).
-  if (!p.a_kcontig || p.b_ncontig) {
-    snprintf(err_buf(), 256,
-             "TF32 path supports K-major operands only (col-major trans_a=T,trans_b=N / row-major N,T)");
     return TB_ERR_UNSUPPORTED;
   }
   const int sms = sms_or_default();

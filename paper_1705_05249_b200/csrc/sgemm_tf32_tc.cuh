@@ -8,7 +8,13 @@
 //   * a 128-byte SWIZZLE_128B row holds 32 FP32 values, so the K block is 32;
 //   * tcgen05.mma.cta_group::1.kind::tf32 consumes K = 8 per instruction
 //     (32 bytes of each K-major row, or 8 K-rows of an MN-major tile);
-//   * MN-major tiles are 32-element (128-byte) chunks of 32 K-rows (4 KB);
+//   * MN-major tiles are 32-element (128-byte) chunks of 32 K-rows (4 KB),
+//     loaded with TMA SWIZZLE_128B_ATOM_32B (32-byte granules swizzled in a
+//     128-byte row) and described to the MMA as layout type 1
+//     (SWIZZLE_128B_BASE32B): LBO 4096 B between 32-element MN chunks, SBO
+//     512 B between 4-row K groups, +1024 B per K8 step — the layout the
+//     hardware accepted in tools/tf32_mn_probe.cu (every 16-byte-swizzle
+//     variant read garbage: FP32 MN-major needs the 32-byte atom);
 //   * the epilogue applies the reference FP32 epilogue and stores FP32.
 // TMA producer only: operands must be 16-byte aligned (checked by the host).
 #pragma once
@@ -47,6 +53,17 @@ __device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t adesc, uin
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+
+// MN-major FP32 operand descriptor (SWIZZLE_128B_BASE32B, layout type 1).
+__device__ __forceinline__ uint64_t umma_desc_mn_tf32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(4096 >> 4) << 16;   // LBO: next 32-element MN chunk
+  d |= static_cast<uint64_t>(512 >> 4) << 32;    // SBO: next 4-row K group
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(1) << 61;           // SWIZZLE_128B_BASE32B
+  return d;
 }
 
 // FP32 variant of epi_store_block: 8 consecutive rows of one column per lane
@@ -177,9 +194,9 @@ __global__ void __launch_bounds__(TfCfg<BN>::THREADS, 1)
           const uint32_t b_addr = smem_u32(sB + s * C::B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < TF_BK / 8; ++kk) {
-            const uint64_t adesc = A_MN ? umma_desc_sw128(a_addr + kk * 1024, 4096, 1024)
+            const uint64_t adesc = A_MN ? umma_desc_mn_tf32(a_addr + kk * 1024)
                                         : umma_desc_sw128(a_addr + kk * 32, 16, 1024);
-            const uint64_t bdesc = B_MN ? umma_desc_sw128(b_addr + kk * 1024, 4096, 1024)
+            const uint64_t bdesc = B_MN ? umma_desc_mn_tf32(b_addr + kk * 1024)
                                         : umma_desc_sw128(b_addr + kk * 32, 16, 1024);
             tc_mma_tf32(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
           }

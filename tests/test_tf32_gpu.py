@@ -21,10 +21,13 @@ def tf32_tol(alpha, beta, a_op, b_op, c):
     return tol + 4 * 2.0 ** -23 * np.abs(beta * c.astype(np.float64)) + 1e-30
 
 
-# K-major operands: col-major T x N and row-major N x T
-@pytest.mark.parametrize("layout,ta,tbn", [("col", "t", "n"), ("row", "n", "t")])
+# every layout: K-major operands (SWIZZLE_128B) and MN-major ones
+# (SWIZZLE_128B_ATOM_32B / descriptor layout SWIZZLE_128B_BASE32B)
+@pytest.mark.parametrize("layout", ["col", "row"])
+@pytest.mark.parametrize("ta,tbn", [("n", "n"), ("n", "t"), ("t", "n"), ("t", "t")])
 @pytest.mark.parametrize("shape", [(512, 640, 256), (300, 200, 132), (1024, 1024, 1024), (4096, 4096, 2048)])
 def test_tf32_matches_float64(ctx, layout, ta, tbn, shape):
+    """Within the TF32 tolerance of the float64 product in every layout."""
     m, n, k = shape
     rng = np.random.default_rng(m + n)
     av = rand_array(rng, (m, k) if ta == "n" else (k, m), Precision.S)
@@ -72,5 +75,31 @@ def test_tf32_rejections(ctx):
         tb.gemm(ctx, Layout.COL_MAJOR, Transpose.YES, Transpose.NO, 5, 5, 5, 1.0, a, a, 0.0, a,
                 a_offset=1, tf32=True)
     b = tb.buffer_alloc(ctx, Precision.S, 256)
-    with pytest.raises(tb.NativeLibraryError, match="K-major operands only"):
-        tb.gemm(ctx, Layout.COL_MAJOR, Transpose.NO, Transpose.NO, 8, 8, 8, 1.0, b, b, 0.0, b, tf32=True)
+    with pytest.raises(tb.NativeLibraryError, match="16-byte aligned"):
+        tb.gemm(ctx, Layout.COL_MAJOR, Transpose.NO, Transpose.NO, 8, 8, 8, 1.0, b, b, 0.0, b, lda=9,
+                tf32=True)
+
+
+@pytest.mark.parametrize("layout", ["col", "row"])
+def test_tf32_all_layouts_agree(ctx, layout):
+    """The MN-major and K-major staging feed the same tensor-core products:
+    the four transpose combinations of one mathematical product agree
+    within the TF32 tolerance of each other (2x) and of float64."""
+    m, n, k = 384, 320, 512
+    rng = np.random.default_rng(21)
+    A = rand_array(rng, (m, k), Precision.S)
+    B = rand_array(rng, (k, n), Precision.S)
+    want = orc.wide_oracle(1.0, A, B, 0.0, None)
+    tol = tf32_tol(1.0, 0.0, A, B, want)
+    outs = []
+    for ta in ("n", "t"):
+        for tbn in ("n", "t"):
+            a = make_buffer(ctx, A if ta == "n" else np.ascontiguousarray(A.T), Precision.S, L[layout])
+            b = make_buffer(ctx, B if tbn == "n" else np.ascontiguousarray(B.T), Precision.S, L[layout])
+            c = tb.buffer_alloc(ctx, Precision.S, m * n)
+            tb.gemm(ctx, L[layout], T[ta], T[tbn], m, n, k, 1.0, a, b, 0.0, c, tf32=True)
+            got = read_mat(c, (m, n), L[layout])
+            assert orc.allclose_tol(got, want, tol), (ta, tbn)
+            outs.append(got)
+    for o in outs[1:]:
+        assert orc.allclose_tol(o, outs[0], tol, scale=2.0)
