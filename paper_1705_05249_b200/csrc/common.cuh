@@ -211,6 +211,17 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo
   return d;
 }
 
+// SWIZZLE_64B operand descriptor (layout type 4): 64-byte rows, 8-row atoms.
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(4) << 61;
+  return d;
+}
+
 // Instruction descriptor, kind::f16: F16 x F16 -> F32.
 //   [4,6) c_format=1 (F32) | [7,10) a_format=0 (F16) | [10,13) b_format=0 |
 //   [15] a_major (1 = MN) | [16] b_major | [17,23) N>>3 | [24,29) M>>4

@@ -399,4 +399,159 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-fed variant for the 32 x 32 x (k <= 32) instances of C4 (arithmetic
+// batch, 16-byte aligned rows and strides).  One 3-D TMA box {32, 32, 4}
+// over (contiguous dim, other dim, batch) per operand per tile lands four
+// instances as [instance][row][64 B] with SWIZZLE_64B — exactly the UMMA
+// SWIZZLE_64B canonical layouts:
+//   K-major  (rows = M or N index, 32 K per 64-byte row): 8-row atoms,
+//            SBO = 512 B; a K16 step advances the start by 32 B;
+//   MN-major (rows = K index, 32 M/N per 64-byte row): instance s is MN
+//            chunk s (LBO = 2048 B), 8-row K groups SBO = 512 B; a K16 step
+//            advances 16 rows = 1024 B.
+// So four instances stack along M of the 128-row tile and side by side
+// along N (BN = 128) as in hgemm_tc_small_kernel, with no per-thread
+// address arithmetic: one elected lane issues 2 TMA loads per tile into a
+// 12-deep ring of 16 KB stages (vs 32 KB cp.async stages filled by 128
+// threads).  Same K16 MMA sequence per element (hg_ksteps), same epilogue:
+// bitwise equal to every other H path.
+struct Hs32Cfg {
+  static constexpr int P = 4, MI = 32, NI = 32, BN = 128;
+  static constexpr int A_BYTES = 128 * 32 * 2, B_BYTES = BN * 32 * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 16 KB
+  static constexpr int STAGES = 12;
+  static constexpr int ACC = 4;
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int EPI_WARPS = 8, PROD_WARP = 8, MMA_WARP = 9;
+  static constexpr int THREADS = 10 * 32;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 1024 + EPI_WARPS * EPI_WARP_FLOATS * 4;
+};
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(Hs32Cfg::THREADS, 1)
+    hgemm_tc_small32_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                                Problem p, int64_t total_tiles) {
+  using C = Hs32Cfg;
+  constexpr int STAGES = C::STAGES, P = C::P, BN = C::BN, ACC = C::ACC, MI = C::MI, NI = C::NI;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_align1024(smem_raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + ACC;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + ACC);
+  float* epi_stage = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES + 1024);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < ACC; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 32 * 4);  // one warp group per tile
+    }
+    fence_mbar_init();
+  }
+  if (warp == C::PROD_WARP && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == C::MMA_WARP) tmem_alloc(tmem_holder, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int m = static_cast<int>(p.m), n = static_cast<int>(p.n);
+
+  if (warp == C::PROD_WARP) {
+    // ===================== producer: 2 TMA boxes per tile =====================
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      mbar_wait(&empty[s], ph ^ 1);
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+        const int z0 = static_cast<int>(t * P);
+        tma_load_3d(sA + s * C::A_BYTES, &tmA, &full[s], 0, 0, z0);
+        tma_load_3d(sB + s * C::B_BYTES, &tmB, &full[s], 0, 0, z0);
+      }
+      __syncwarp();
+      if (++s == STAGES) { s = 0; ph ^= 1; }
+    }
+  } else if (warp == C::MMA_WARP) {
+    // ===================== MMA issuer =====================
+    constexpr uint32_t idesc = umma_idesc_f16(128, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+    const int ksteps = hg_ksteps(p.k, 0);
+    int s = 0, acc = 0;
+    uint32_t ph = 0, aph = 0;
+    for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], aph ^ 1);
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+      const uint32_t a_addr = smem_u32(sA + s * C::A_BYTES);
+      const uint32_t b_addr = smem_u32(sB + s * C::B_BYTES);
+      if (elect_one()) {
+#pragma unroll 1
+        for (int kk = 0; kk < ksteps; ++kk) {
+          const uint64_t ad = A_MN ? umma_desc_sw64(a_addr + kk * 1024, 2048, 512)
+                                   : umma_desc_sw64(a_addr + kk * 32, 16, 512);
+          const uint64_t bd = B_MN ? umma_desc_sw64(b_addr + kk * 1024, 2048, 512)
+                                   : umma_desc_sw64(b_addr + kk * 32, 16, 512);
+          tc_mma_f16(d_tmem, ad, bd, idesc, kk != 0 ? 1u : 0u);
+        }
+        tc_commit(&empty[s]);
+        tc_commit(&tfull[acc]);
+      }
+      __syncwarp();
+      if (++s == STAGES) { s = 0; ph ^= 1; }
+      if (++acc == ACC) { acc = 0; aph ^= 1; }
+    }
+  } else if (warp < C::EPI_WARPS) {
+    // ===================== epilogue (as hgemm_tc_small_kernel) =====================
+    const int quad = warp & 3;
+    const int grp = warp >> 2;
+    const int slot = (quad * 32) / MI;
+    int64_t seq = grp;
+    for (int64_t t = blockIdx.x + static_cast<int64_t>(grp) * gridDim.x; t < total_tiles;
+         t += 2 * static_cast<int64_t>(gridDim.x), seq += 2) {
+      const int acc = static_cast<int>(seq % ACC);
+      const uint32_t aph = static_cast<uint32_t>((seq / ACC) & 1);
+      const int64_t zi = t * P + slot;
+      const bool inst_ok = zi < p.batch;
+      Epi epi;
+      epi.alpha = inst_ok ? inst_alpha(p, zi) : 0.0f;
+      epi.beta = inst_ok ? inst_beta(p, zi) : 0.0f;
+      epi.skip_ab = (epi.alpha == 0.0f);
+      __half* Cz = static_cast<__half*>(p.c) + (inst_ok ? inst_off(p.c_off, p.stride_c, p.c_offs, zi) : 0);
+      const int row0 = quad * 32 - slot * MI;
+      const int rows_valid = inst_ok ? min(32, m - row0) : 0;
+      float* stage = epi_stage + warp * EPI_WARP_FLOATS;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                             static_cast<uint32_t>(acc * BN + slot * NI);
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(t_row, v);
+      tmem_ld_wait();
+      if (rows_valid > 0)
+        epi_store_block<32>(stage, v, Cz + row0, p.ldc, rows_valid, n, epi, lane);
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == C::MMA_WARP) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
 }  // namespace tb

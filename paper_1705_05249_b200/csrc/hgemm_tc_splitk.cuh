@@ -18,6 +18,14 @@
 // KS x 256 epilogue threads have written their partials (release.cluster
 // arrivals, acquire.cluster wait), red_empty[r] when all of them have finished
 // reading, so a buffer is rewritten only after every reader is done.
+//
+// The 64 KB partial buffer ALIASES the first ring stages: a tile's partial is
+// written after its last MMA retired (every stage of this tile consumed),
+// and the producer starts the loads of a CTA's next tile only after
+// red_empty of the previous one (every peer finished reading), so the ring is
+// 7 stages deep instead of 5 + a separate buffer — the single-tile CTAs of
+// these shapes are load-latency bound, and bytes in flight per SM are what
+// they run on.
 #pragma once
 
 #include "hgemm_tc.cuh"
@@ -32,7 +40,7 @@ constexpr int SK_RED_LD = HG_BM;
 
 template <bool TMA>
 struct SkCfg {
-  static constexpr int STAGES = 5;
+  static constexpr int STAGES = 7;
   static constexpr int A_BYTES = HG_BM * HG_BK * 2;   // 16 KB
   static constexpr int B_BYTES = SK_BN * HG_BK * 2;   // 16 KB
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -44,8 +52,9 @@ struct SkCfg {
   static constexpr int THREADS = (MMA_WARP + 1) * 32;
   static constexpr int EPI_THREADS = EPI_WARPS * 32;
   static constexpr int BAR_BYTES = 1024;
-  static constexpr int RED_BYTES = SK_BN * SK_RED_LD * 4;
-  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + BAR_BYTES + RED_BYTES;
+  static constexpr int RED_BYTES = SK_BN * SK_RED_LD * 4;  // aliases ring stages (A region)
+  static_assert(RED_BYTES <= STAGES * A_BYTES, "partial buffer inside the A ring");
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + BAR_BYTES;
   static_assert(SMEM_BYTES <= 232448, "fits the 227 KB opt-in shared memory");
 };
 
@@ -106,7 +115,7 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
   uint64_t* red_full = tempty + 2;
   uint64_t* red_empty = red_full + 1;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(red_empty + 1);
-  float* red = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES + C::BAR_BYTES);
+  float* red = reinterpret_cast<float*>(smem);  // aliases ring stages (see above)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -148,8 +157,13 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
     // ======================= producer (own K range) =======================
     int s = 0;
     uint32_t ph = 0;
+    uint32_t tph = 0;  // parity of red_empty for the previous tile
     if (TMA) {
       for (int64_t t = cluster_id; t < total_tiles; t += n_clusters) {
+        if (t != cluster_id) {  // the ring holds the previous tile's partial until every peer read it
+          sk_wait_cluster(red_empty, tph);
+          tph ^= 1;
+        }
         int64_t z; int mt, nt;
         tile_coords(t, tiles_m, tiles_n, group_m, z, mt, nt);
         const int m0 = mt * HG_BM, n0 = nt * BN, zz = static_cast<int>(z);
@@ -180,6 +194,10 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
     } else {
       const int tid = threadIdx.x - C::PROD_WARP0 * 32;  // 0..127
       for (int64_t t = cluster_id; t < total_tiles; t += n_clusters) {
+        if (t != cluster_id) {
+          sk_wait_cluster(red_empty, tph);
+          tph ^= 1;
+        }
         int64_t z; int mt, nt;
         tile_coords(t, tiles_m, tiles_n, group_m, z, mt, nt);
         const int64_t m0 = static_cast<int64_t>(mt) * HG_BM, n0 = static_cast<int64_t>(nt) * BN;

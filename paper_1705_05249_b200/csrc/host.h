@@ -71,7 +71,7 @@ int ensure_smem(SmemAttr& st, K kern, int bytes) {
 int make_map(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t batch, uint64_t ld,
              uint64_t stride, uint32_t box0, uint32_t box1,
              CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT16, uint64_t es = 2,
-             CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B);
+             CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B, uint32_t box2 = 1);
 
 inline bool aligned_elems(const void* base, int64_t off, int64_t elem, int64_t vec_bytes) {
   return ((reinterpret_cast<uintptr_t>(base) + off * elem) % vec_bytes) == 0;

@@ -101,7 +101,7 @@ static EncodeTiledFn get_encode_fn() {
 
 int make_map(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t batch, uint64_t ld,
              uint64_t stride, uint32_t box0, uint32_t box1, CUtensorMapDataType dt, uint64_t es,
-             CUtensorMapSwizzle swizzle) {
+             CUtensorMapSwizzle swizzle, uint32_t box2) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) {
     snprintf(g_last_err, sizeof(g_last_err), "cuTensorMapEncodeTiled entry point unavailable");
@@ -111,7 +111,7 @@ int make_map(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint6
   uint64_t zstride = stride * es;
   if (batch <= 1) zstride = ((ld * d1 * es) + 15) / 16 * 16;
   cuuint64_t strides[2] = {ld * es, zstride};
-  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t box[3] = {box0, box1, box2};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
