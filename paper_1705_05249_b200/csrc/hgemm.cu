@@ -208,14 +208,19 @@ int launch_hsk(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm, int
   }
   const int64_t clusters = total < max_clusters[dev][ks] ? total : max_clusters[dev][ks];
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * ks));
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tbm, p, tiles_m, tiles_n, cfg_group_m(c, 16), total);
+  // partials through L2 when a workspace is available (sized for a grid of
+  // up to the SM count, so one allocation per stream serves every shape)
+  float* ws = static_cast<float*>(
+      splitk_workspace(c.stream, static_cast<size_t>(sms_or_default()) * SK_WS_FLOATS * sizeof(float)));
+  if (cfg.gridDim.x > static_cast<unsigned>(sms_or_default())) ws = nullptr;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tbm, p, tiles_m, tiles_n, cfg_group_m(c, 16), total, ws);
   if (e != cudaSuccess) {
     set_err("hgemm_tc_splitk launch", e);
     return TB_ERR_CUDA;
   }
   char name[64];
-  snprintf(name, sizeof(name), "hgemm_tc_splitk%d_%s_128x128_%c%c%s", ks, TMA ? "tma" : "ldg", AMN ? 'm' : 'k',
-           BMN ? 'n' : 'k', (!TMA && !VEC) ? "_scalar" : "");
+  snprintf(name, sizeof(name), "hgemm_tc_splitk%d_%s_128x128_%c%c%s%s", ks, TMA ? "tma" : "ldg", AMN ? 'm' : 'k',
+           BMN ? 'n' : 'k', (!TMA && !VEC) ? "_scalar" : "", ws ? "" : "_dsmem");
   record(name, cfg.gridDim, cfg.blockDim, ks, Cfg::SMEM_BYTES, total);
   return check_launch("hgemm_tc_splitk launch");
 }
@@ -333,3 +338,11 @@ int launch_hscale(const Call& c) {
 
 }  // namespace host
 }  // namespace tb
+
+#ifdef TB_SPLITK_TIMING
+// Debug builds only (tools/splitk_timeline.py): copy the split-K kernel's
+// per-CTA %globaltimer stamps to the host.
+extern "C" int tb_debug_splitk_times(unsigned long long* host, int count) {
+  return cudaMemcpyFromSymbol(host, tb::tb_sk_times, sizeof(unsigned long long) * count) == cudaSuccess ? 0 : 1;
+}
+#endif

@@ -19,6 +19,16 @@
 // arrivals, acquire.cluster wait), red_empty[r] when all of them have finished
 // reading, so a buffer is rewritten only after every reader is done.
 //
+// Exchange medium: with a workspace (ws != nullptr; one 64 KB slot per CTA,
+// allocated per stream by the host, tbgemm.cu splitk_workspace) the
+// partials go through L2 — TMEM -> registers -> st.global.cg, peers read
+// with ld.global.cg after the cluster barrier.  DSMEM runs at ~20 B/cycle
+// per SM (B300_MICROARCH "DSMEM BW", producer pays the smem port): reading
+// 3 peers' 16 KB slices took 3.6 us of a 23 us C3 call (%globaltimer
+// timeline, tools/splitk_timeline.py).  Without a workspace (a stream seen
+// first under graph capture) the shared-memory buffer below is read
+// through DSMEM instead; the sum order is the same, so results are too.
+//
 // The 64 KB partial buffer ALIASES the first ring stages: a tile's partial is
 // written after its last MMA retired (every stage of this tile consumed),
 // and the producer starts the loads of a CTA's next tile only after
@@ -32,11 +42,29 @@
 
 namespace tb {
 
+// Optional per-CTA timeline (build with -DTB_SPLITK_TIMING; tools/splitk_timeline.py):
+// %globaltimer stamps of the kernel's phases in tb_sk_times[block * 16 + i].
+#ifdef TB_SPLITK_TIMING
+__device__ unsigned long long tb_sk_times[2048 * 16];
+#define SK_STAMP(i)                                                              \
+  do {                                                                           \
+    unsigned long long _t;                                                       \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                      \
+    tb_sk_times[static_cast<size_t>(blockIdx.x) * 16 + (i)] = _t;                \
+  } while (0)
+#else
+#define SK_STAMP(i) \
+  do {              \
+  } while (0)
+#endif
+
 constexpr int SK_BN = 128;
 // Floats per column of the partial buffer.  Unpadded: the row-per-lane
 // writes are conflict-free, the float4 reduction reads 2-way; the 4 KB saved
 // buys a 5th pipeline stage (single-tile CTAs are load-latency bound).
 constexpr int SK_RED_LD = HG_BM;
+// Floats of one CTA's partial slot in the global split-K workspace.
+constexpr int SK_WS_FLOATS = SK_BN * SK_RED_LD;
 
 template <bool TMA>
 struct SkCfg {
@@ -80,6 +108,14 @@ __device__ __forceinline__ uint32_t sk_mapa(uint32_t local, uint32_t rank) {
 __device__ __forceinline__ void sk_arrive_remote(uint32_t bar_cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
 }
+// One cluster-scope fence, then relaxed arrivals on every rank's barrier: a
+// release arrive per rank compiled to a full MEMBAR.ALL.GPU each, and after
+// the tile's global C stores those waited for the stores to drain (ncu /
+// %globaltimer: 5.4 us of the reduction phase at C3).
+__device__ __forceinline__ void sk_fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+__device__ __forceinline__ void sk_arrive_remote_relaxed(uint32_t bar_cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
+}
 __device__ __forceinline__ void sk_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -89,19 +125,22 @@ __device__ __forceinline__ void sk_wait_cluster(uint64_t* bar, uint32_t parity) 
       "r"(parity)
       : "memory");
 }
+// DSMEM load.  volatile keeps it ordered after the cluster-barrier waits
+// (volatile asm with "memory" clobbers); no clobber of its own, so a run of
+// these loads issues back to back and their latencies overlap.
 __device__ __forceinline__ float4 sk_ld_cluster_f4(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(addr)
-               : "memory");
+               : "r"(addr));
   return v;
 }
 
 template <bool TMA, bool A_MN, bool B_MN, bool VEC>
 __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
     hgemm_tc_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                           Problem p, int tiles_m, int tiles_n, int group_m, int64_t total_tiles) {
+                           Problem p, int tiles_m, int tiles_n, int group_m, int64_t total_tiles,
+                           float* __restrict__ ws) {
   using C = SkCfg<TMA>;
   constexpr int STAGES = C::STAGES, BN = SK_BN;
   extern __shared__ uint8_t smem_raw[];
@@ -143,9 +182,11 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
   }
   if (warp == C::MMA_WARP) tmem_alloc(tmem_holder, C::TMEM_COLS);
   tc_fence_before();
+  if (threadIdx.x == 0) SK_STAMP(0);
   sk_cluster_sync();  // barriers of every CTA initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  if (threadIdx.x == 0) SK_STAMP(1);
 
   const int nkb = static_cast<int>((p.k + HG_BK - 1) / HG_BK);
   // K blocks are dealt round-robin (rank r: kb = r, r+KS, ...): the KS CTAs
@@ -170,6 +211,7 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
         for (int kb = static_cast<int>(rank); kb < nkb; kb += static_cast<int>(ks)) {
           mbar_wait(&empty[s], ph ^ 1);
           if (elect_one()) {
+            if (kb == static_cast<int>(rank) && t == cluster_id) SK_STAMP(2);
             mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
             const int k0 = kb * HG_BK;
             uint8_t* a_dst = sA + s * C::A_BYTES;
@@ -233,6 +275,8 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
       for (int kb = static_cast<int>(rank); kb < nkb; kb += static_cast<int>(ks)) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
+        if (lane == 0 && t == cluster_id && kb == static_cast<int>(rank)) SK_STAMP(3);
+        if (lane == 0 && t == cluster_id && kb + static_cast<int>(ks) >= nkb) SK_STAMP(4);
         const uint32_t a_addr = smem_u32(sA + s * C::A_BYTES);
         const uint32_t b_addr = smem_u32(sB + s * C::B_BYTES);
         const int ksteps = hg_ksteps(p.k, kb);
@@ -256,6 +300,10 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
     const int row_base = static_cast<int>(rank) * rp;
     const uint32_t red_s = smem_u32(red);
     const uint32_t rf_local = smem_u32(red_full), re_local = smem_u32(red_empty);
+    // global-workspace exchange (ws != nullptr): this CTA's partial slot and
+    // rank 0's slot of the cluster (slots are consecutive per cluster)
+    float* ws_mine = ws ? ws + static_cast<size_t>(blockIdx.x) * SK_WS_FLOATS : nullptr;
+    const float* ws_base = ws ? ws + static_cast<size_t>(blockIdx.x - rank) * SK_WS_FLOATS : nullptr;
     int acc = 0;
     uint32_t aph = 0, rph = 0;
     for (int64_t t = cluster_id; t < total_tiles; t += n_clusters) {
@@ -267,6 +315,7 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
       sk_wait_cluster(red_empty, rph ^ 1);  // every reader of the previous tile is done
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
+      if (et == 0 && t == cluster_id) SK_STAMP(5);
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(acc * BN);
       const int row = quad * 32 + lane;
 #pragma unroll 1
@@ -275,15 +324,23 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
         tmem_ld_32x32b_x32(t_row + cb * 32, v);
         tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) red[(cb * 32 + j) * SK_RED_LD + row] = __uint_as_float(v[j]);
+        if (ws_mine != nullptr) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) __stcg(ws_mine + (cb * 32 + j) * SK_RED_LD + row, __uint_as_float(v[j]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) red[(cb * 32 + j) * SK_RED_LD + row] = __uint_as_float(v[j]);
+        }
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);  // TMEM buffer free for the next tile's MMAs
       if (++acc == 2) { acc = 0; aph ^= 1; }
-      for (uint32_t q = 0; q < ks; ++q) sk_arrive_remote(sk_mapa(rf_local, q));
+      sk_fence_cluster();  // the partial is visible cluster-wide before any arrival
+      for (uint32_t q = 0; q < ks; ++q) sk_arrive_remote_relaxed(sk_mapa(rf_local, q));
 
       // (2) reduce rows [row_base, row_base + rp) over all ranks, in rank order
       sk_wait_cluster(red_full, rph);
+      if (et == 0 && t == cluster_id) SK_STAMP(6);
       Epi epi;
       epi.alpha = inst_alpha(p, z);
       epi.beta = inst_beta(p, z);
@@ -291,26 +348,64 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
       __half* Cz = static_cast<__half*>(p.c) + inst_off(p.c_off, p.stride_c, p.c_offs, z);
       const int n_left = static_cast<int>(min64(BN, p.n - n0));
       const bool vec_ok = ((reinterpret_cast<uintptr_t>(Cz) & 15) == 0) && ((p.ldc & 7) == 0);
-      const int groups = (rp / 8) * BN;  // (8-row group, column) items
-      for (int it = et; it < groups; it += C::EPI_THREADS) {
+      const int groups = (rp / 8) * BN;  // (8-row group, column) items: <= 4 per thread (KS >= 2)
+      constexpr int MAXIT = 4;
+      float xs[MAXIT][8];
+      // (2a) every rank's partial values first (up to 16 loads in flight per
+      // item), summed in rank order 0..KS-1 (deterministic)
+#pragma unroll
+      for (int j = 0; j < MAXIT; ++j) {
+        const int it = et + j * C::EPI_THREADS;
+        if (it >= groups) break;
         const int col = it / (rp / 8);
         const int r0 = row_base + (it % (rp / 8)) * 8;
         const uint32_t off = red_s + static_cast<uint32_t>((col * SK_RED_LD + r0) * 4);
-        float x[8];
-        {
-          const float4 a0 = sk_ld_cluster_f4(sk_mapa(off, 0));
-          const float4 a1 = sk_ld_cluster_f4(sk_mapa(off + 16, 0));
-          x[0] = a0.x; x[1] = a0.y; x[2] = a0.z; x[3] = a0.w;
-          x[4] = a1.x; x[5] = a1.y; x[6] = a1.z; x[7] = a1.w;
+        float4 pv[8][2];
+        if (ws_base != nullptr) {
+          const float* src = ws_base + (col * SK_RED_LD + r0);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (q < static_cast<int>(ks)) {
+              pv[q][0] = __ldcg(reinterpret_cast<const float4*>(src + q * SK_WS_FLOATS));
+              pv[q][1] = __ldcg(reinterpret_cast<const float4*>(src + q * SK_WS_FLOATS + 4));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (q < static_cast<int>(ks)) {
+              pv[q][0] = sk_ld_cluster_f4(sk_mapa(off, q));
+              pv[q][1] = sk_ld_cluster_f4(sk_mapa(off + 16, q));
+            }
+          }
         }
-        for (uint32_t q = 1; q < ks; ++q) {
-          const float4 b0 = sk_ld_cluster_f4(sk_mapa(off, q));
-          const float4 b1 = sk_ld_cluster_f4(sk_mapa(off + 16, q));
-          x[0] = __fadd_rn(x[0], b0.x); x[1] = __fadd_rn(x[1], b0.y);
-          x[2] = __fadd_rn(x[2], b0.z); x[3] = __fadd_rn(x[3], b0.w);
-          x[4] = __fadd_rn(x[4], b1.x); x[5] = __fadd_rn(x[5], b1.y);
-          x[6] = __fadd_rn(x[6], b1.z); x[7] = __fadd_rn(x[7], b1.w);
+        float* x = xs[j];
+        x[0] = pv[0][0].x; x[1] = pv[0][0].y; x[2] = pv[0][0].z; x[3] = pv[0][0].w;
+        x[4] = pv[0][1].x; x[5] = pv[0][1].y; x[6] = pv[0][1].z; x[7] = pv[0][1].w;
+#pragma unroll
+        for (int q = 1; q < 8; ++q) {
+          if (q < static_cast<int>(ks)) {
+            x[0] = __fadd_rn(x[0], pv[q][0].x); x[1] = __fadd_rn(x[1], pv[q][0].y);
+            x[2] = __fadd_rn(x[2], pv[q][0].z); x[3] = __fadd_rn(x[3], pv[q][0].w);
+            x[4] = __fadd_rn(x[4], pv[q][1].x); x[5] = __fadd_rn(x[5], pv[q][1].y);
+            x[6] = __fadd_rn(x[6], pv[q][1].z); x[7] = __fadd_rn(x[7], pv[q][1].w);
+          }
         }
+      }
+      if (et == 0 && t == cluster_id) SK_STAMP(9);
+      // (2b) done reading every rank's partial of this tile: release the
+      // buffers before the (slow to drain) global stores
+      sk_fence_cluster();
+      for (uint32_t q = 0; q < ks; ++q) sk_arrive_remote_relaxed(sk_mapa(re_local, q));
+      if (et == 0 && t == cluster_id) SK_STAMP(10);
+      // (2c) epilogue and 16-byte stores
+#pragma unroll
+      for (int j = 0; j < MAXIT; ++j) {
+        const int it = et + j * C::EPI_THREADS;
+        if (it >= groups) break;
+        const int col = it / (rp / 8);
+        const int r0 = row_base + (it % (rp / 8)) * 8;
+        const float* x = xs[j];
         const int64_t grow = m0 + r0;
         if (col >= n_left || grow >= p.m) continue;
         __half* dst = Cz + (n0 + col) * p.ldc + grow;
@@ -343,8 +438,7 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
           }
         }
       }
-      // (3) done reading every rank's partial of this tile
-      for (uint32_t q = 0; q < ks; ++q) sk_arrive_remote(sk_mapa(re_local, q));
+      if (et == 0 && t == cluster_id) SK_STAMP(7);
       rph ^= 1;
     }
   }
@@ -356,6 +450,7 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
     tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
   sk_cluster_sync();  // no CTA leaves while a peer may still read its partials
+  if (threadIdx.x == 0) SK_STAMP(8);
 }
 
 }  // namespace tb

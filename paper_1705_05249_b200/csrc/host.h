@@ -79,6 +79,8 @@ inline bool aligned_elems(const void* base, int64_t off, int64_t elem, int64_t v
 
 // Wave-barrier counter slot for (device, stream), or nullptr (tbgemm.cu).
 unsigned int* wave_counter(cudaStream_t stream);
+// Split-K partial workspace of `bytes` for (device, stream), or nullptr (tbgemm.cu).
+void* splitk_workspace(cudaStream_t stream, size_t bytes);
 
 // Dispatchers.
 int dispatch_sgemm(const Call& c);                                   // sgemm.cu

@@ -172,6 +172,43 @@ unsigned int* wave_counter(cudaStream_t stream) {
   return wp.base + 64 * wp.used++;
 }
 
+// Split-K partial workspace (hgemm_tc_splitk.cuh): one slot of `slot_bytes`
+// per CTA of a grid of at most the SM count, per (device, stream), allocated
+// on first use outside stream capture.  nullptr: the kernel exchanges
+// partials through DSMEM instead (same summation order, same results).
+constexpr int kWsSlots = 16;
+struct WsPool {
+  cudaStream_t streams[kWsSlots] = {};
+  void* ptr[kWsSlots] = {};
+  int used = 0;
+};
+static std::mutex g_ws_mu;
+static WsPool g_ws[64];
+
+void* splitk_workspace(cudaStream_t stream, size_t bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(g_ws_mu);
+  WsPool& wp = g_ws[dev];
+  for (int i = 0; i < wp.used; ++i)
+    if (wp.streams[i] == stream) return wp.ptr[i];
+  if (wp.used == kWsSlots) return nullptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  wp.streams[wp.used] = stream;
+  wp.ptr[wp.used] = p;
+  ++wp.used;
+  return p;
+}
+
 }  // namespace host
 }  // namespace tb
 
