@@ -20,7 +20,9 @@ Contents (each function cites what it restates):
 * ``port_gemm_strided_batched`` — the per-instance loop of
   _gemm_batched_core (extras.py:188-286) on the sequential backend.
 * ``seqk_gemm`` — ctypes wrapper of oracle/gemm_seqk.c (sequential-k FMA
-  chain; bit-exact checker for the GPU SGEMM contract).
+  chain; bit-exact checker for the GPU SGEMM contract); ``seqk_gemm_split``
+  — the same chain cut into the GPU's split-K ranges and summed in rank
+  order (bit-exact checker for the split-K SGEMM route).
 * ``port_im2col`` — the reference's ``im2col`` gather (extras.py:56-109):
   index grids per (channel, ky, kx) row and (oy, ox) column, zero outside the
   image, written column-major with ld = rows.  Pinned bitwise to
@@ -288,6 +290,34 @@ def seqk_gemm_strided_batched(prec, row_major, trans_a, trans_b, m, n, k, alpha,
         float(beta), _ptr(c), c_offset, ldc, stride_c, batch)
     if rc:
         raise ValueError("oracle_gemm_strided_batched rejected its arguments")
+
+
+def seqk_gemm_split(prec: str, row_major: bool, trans_a: bool, trans_b: bool, m, n, k, alpha,
+                    a: np.ndarray, a_offset, lda, b: np.ndarray, b_offset, ldb, beta, c: np.ndarray,
+                    c_offset, ldc, ks: int, stage: int = 32) -> None:
+    """The GPU's deterministic split-K SGEMM (csrc/sgemm_tma.cuh, KS > 1):
+    rank r runs the sequential-k chain over K stages [r*kt, (r+1)*kt) of
+    `stage` elements (kt = ceil(ceil(k/stage)/ks)), the partials are added in
+    rank order with FP32 roundings, then the reference epilogue (alpha*acc,
+    + beta*C as separately rounded FP32 ops; compute.py:408-412).  Row-major
+    and untransposed operands only (what the split route serves in tests)."""
+    assert prec == "S" and row_major and not trans_a and not trans_b
+    kt = -(-(-(-k // stage)) // ks)
+    total = None
+    for r in range(ks):
+        k0, k1 = min(k, r * kt * stage), min(k, (r + 1) * kt * stage)
+        part = np.zeros(m * n, np.float32)
+        if k1 > k0:
+            seqk_gemm("S", True, False, False, m, n, k1 - k0, 1.0, a, a_offset + k0, lda, b,
+                      b_offset + k0 * ldb, ldb, 0.0, part, 0, n)
+        total = part if total is None else (total + part).astype(np.float32)
+    cv = logical(c, c_offset, m, n, ldc, True)
+    al, be = np.float32(alpha), np.float32(beta)
+    acc = total.reshape(m, n)
+    out = (al * acc).astype(np.float32)
+    if be != 0:
+        out = (out + (be * cv.astype(np.float32)).astype(np.float32)).astype(np.float32)
+    cv[...] = out
 
 
 def port_im2col(image_flat: np.ndarray, im_offset: int, channels: int, height: int, width: int,

@@ -10,7 +10,7 @@ namespace tb {
 namespace host {
 namespace {
 
-template <int BM, int BN, int TM, int TN, int ST, bool AMN, bool BMN, bool XP = false, int MINB = 2>
+template <int BM, int BN, int TM, int TN, int ST, bool AMN, bool BMN, bool XP = false, int MINB = 2, int KS = 1>
 int launch_stma(const Call& c) {
   using Cfg = TmaSgemmCfg<BM, BN, 32, TM, TN, ST, AMN, BMN, XP>;
   const Problem& p = c.p;
@@ -30,15 +30,36 @@ int launch_stma(const Call& c) {
   const int tiles_n = static_cast<int>((p.n + BN - 1) / BN);
   const int64_t blocks = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
   if (blocks > 0x7fffffffLL) return TB_ERR_INVALID;
-  auto kern = sgemm_tma_kernel<BM, BN, 32, TM, TN, ST, AMN, BMN, MINB, XP>;
+  if (blocks * KS > 0x7fffffffLL) return TB_ERR_INVALID;
+  auto kern = sgemm_tma_kernel<BM, BN, 32, TM, TN, ST, AMN, BMN, MINB, XP, KS>;
   static SmemAttr attr;  // per instantiation, per device
   if (int rc2 = ensure_smem(attr, kern, Cfg::SMEM_BYTES)) return rc2;
-  dim3 grid(static_cast<unsigned>(blocks)), block(Cfg::NT);
-  kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, cfg_group_m(c, 8));
+  dim3 grid(static_cast<unsigned>(blocks * KS)), block(Cfg::NT);
+  if constexpr (KS == 1) {
+    kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, cfg_group_m(c, 8));
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeClusterDimension;
+    la[0].val.clusterDim.x = KS;
+    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.z = 1;
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cfg.stream = c.stream;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tbm, p, tiles_m, tiles_n, cfg_group_m(c, 8));
+    if (e != cudaSuccess) {
+      set_err("sgemm_tma split-K launch", e);
+      return TB_ERR_CUDA;
+    }
+  }
   char name[64];
-  snprintf(name, sizeof(name), "sgemm_tma_%dx%dx32_%dx%d_%c%c%s", BM, BN, TM, TN, AMN ? 'm' : 'k', BMN ? 'n' : 'k',
-           (Cfg::A_T || Cfg::B_T) ? "_xp" : "");
-  record(name, grid, block, 1, Cfg::SMEM_BYTES, blocks);
+  snprintf(name, sizeof(name), "sgemm_tma_%dx%dx32_%dx%d_%c%c%s%s", BM, BN, TM, TN, AMN ? 'm' : 'k',
+           BMN ? 'n' : 'k', (Cfg::A_T || Cfg::B_T) ? "_xp" : "", KS == 2 ? "_splitk2" : (KS == 4 ? "_splitk4" : ""));
+  record(name, grid, block, KS, Cfg::SMEM_BYTES, blocks);
   return check_launch("sgemm_tma launch");
 }
 
@@ -52,6 +73,34 @@ int big_tiles(const Call& c, bool amn, bool bmn) {
   if (bmn) return launch_stma<64, 128, 8, 8, 2, false, true, true>(c);
   return launch_stma<64, 128, 8, 8, 2, false, false, true>(c);
 }
+// Deterministic split-K for the 128x64 tile (clusters of KS CTAs, DSMEM
+// reduction in rank order; sgemm_tma.cuh).  KS is a pure function of the
+// per-instance shape (m, n, k) and the SM count — never of the batch — so
+// single, batched and looped calls agree bitwise: when one instance's
+// 128x64 tiles fill less than half the SMs, the smallest KS in {2, 4} that
+// brings them to at least one wave (and at most two CTAs per SM), keeping
+// >= 8 K stages per rank.  Measured (tools/route_probe.py): C3 (4096, 128,
+// 9216): 64 tiles, KS = 4: 265 -> 221 us; C1 (1024^3, 128 tiles) split in
+// two ran slower than unsplit (59.4 vs 55.8 us), hence the half-wave bound.
+// Returns 1 when K is not split.
+int sgemm_split_ks(const Problem& p) {
+  const int sms = sms_or_default();
+  const int64_t t1 = ((p.m + 127) / 128) * ((p.n + 63) / 64);
+  const int64_t ktiles = (p.k + 31) / 32;
+  if (2 * t1 > sms) return 1;
+  for (int ks = 2; ks <= 4; ks *= 2)
+    if (t1 * ks >= sms && t1 * ks <= 2 * sms && ktiles >= 8 * ks) return ks;
+  return 1;
+}
+
+template <int KS>
+int tiles_128x64_split(const Call& c, bool amn, bool bmn) {
+  if (amn && bmn) return launch_stma<128, 64, 4, 8, 4, true, true, false, 2, KS>(c);
+  if (amn) return launch_stma<128, 64, 4, 8, 4, true, false, false, 2, KS>(c);
+  if (bmn) return launch_stma<128, 64, 4, 8, 4, false, true, false, 2, KS>(c);
+  return -1;
+}
+
 int tiles_128x64(const Call& c, bool amn, bool bmn) {
   if (amn && bmn) return launch_stma<128, 64, 4, 8, 4, true, true>(c);
   if (amn) return launch_stma<128, 64, 4, 8, 4, true, false>(c);
@@ -110,6 +159,11 @@ int dispatch_sgemm_tma(const Call& c, int tile, int mwg, int nwg) {
     return -1;
   }
   if (tile == 3) return tiles_32x32(c, amn, bmn);
+  if (tile == 0 && (amn || bmn) && !(c.flags & TB_FLAG_NO_SPLITK)) {
+    const int ks = sgemm_split_ks(p);
+    if (ks == 2) return tiles_128x64_split<2>(c, amn, bmn);
+    if (ks == 4) return tiles_128x64_split<4>(c, amn, bmn);
+  }
   const int sms = sms_or_default();
   const int64_t tiles128 = ((p.m + 127) / 128) * ((p.n + 127) / 128) * p.batch;
   // Measured on B200 (tools/sgemm_ms_bench.cu): with >= 4 waves of 128x128

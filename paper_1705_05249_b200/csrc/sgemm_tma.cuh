@@ -75,7 +75,19 @@ __device__ __forceinline__ void outer_ffma2_n(float2 (&acc2)[TM][TN / 2], const 
                                acc2[i][j2]);
 }
 
-template <int BM, int BN, int BK, int TM, int TN, int STAGES, bool A_MN, bool B_MN, int MINB, bool XP = false>
+// KS > 1: deterministic split-K over a thread-block cluster of KS CTAs
+// (launched with cluster dims (KS,1,1)): rank r runs the 32-deep K stages
+// [r*kt_per, (r+1)*kt_per) of the tile (kt_per = ceil(ktiles / KS)), i.e.
+// the ascending-k FMA chain of its K range from 0; ranks 1.. park their
+// accumulators in their own shared memory, and rank 0 reads them through
+// DSMEM and adds them in rank order — ((p0 + p1) + p2) + p3, one rounded
+// FP32 add each — before the reference epilogue.  The split is chosen from
+// (m, n, k) only (sgemm_tma.cu), so single, batched and looped calls of a
+// shape agree bitwise; against the sequential-k oracle the result is the
+// same chain cut at the rank boundaries (tests: oracle seqk over each K
+// range, then the rank-order sum).
+template <int BM, int BN, int BK, int TM, int TN, int STAGES, bool A_MN, bool B_MN, int MINB, bool XP = false,
+          int KS = 1>
 __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, B_MN, XP>::NT, MINB)
     sgemm_tma_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                      Problem p, int tiles_m, int tiles_n, int group_m) {
@@ -91,12 +103,15 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
   const int tid = threadIdx.x;
   const int lane = tid % 32;
 
-  // tile coordinates (grouped rasterisation), one tile per CTA
+  // tile coordinates (grouped rasterisation), one tile per CTA (per
+  // cluster of KS CTAs when K is split)
   const int64_t per_inst = static_cast<int64_t>(tiles_m) * tiles_n;
-  const int z = static_cast<int>(blockIdx.x / per_inst);
+  const int64_t tile_id = blockIdx.x / KS;
+  const int krank = KS > 1 ? static_cast<int>(blockIdx.x % KS) : 0;
+  const int z = static_cast<int>(tile_id / per_inst);
   int mt, nt;
   {
-    const int r = static_cast<int>(blockIdx.x - z * per_inst);
+    const int r = static_cast<int>(tile_id - z * per_inst);
     const int group_size = group_m * tiles_n;
     const int g = r / group_size;
     const int first_m = g * group_m;
@@ -109,7 +124,11 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
   const int rows_m = static_cast<int>(min64(BM, p.m - m0));
   const int cols_n = static_cast<int>(min64(BN, p.n - n0));
   const int k_total = static_cast<int>(min64(p.k, 0x7fffffff));
-  const int ktiles = (k_total + BK - 1) / BK;
+  const int ktiles_all = (k_total + BK - 1) / BK;
+  // this CTA's K stages [kt0, kt0 + ktiles)
+  const int kt_per = KS > 1 ? (ktiles_all + KS - 1) / KS : ktiles_all;
+  const int kt0 = min(ktiles_all, krank * kt_per);
+  const int ktiles = min(ktiles_all, kt0 + kt_per) - kt0;
 
   if (tid == 0) {
     tma_prefetch_desc(&tmap_a);
@@ -122,15 +141,16 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
   }
   __syncthreads();
 
-  auto issue = [&](int t) {  // stage t -> slot t % STAGES (tid 0 only)
+  auto issue = [&](int t) {  // local stage t -> slot t % STAGES (tid 0 only)
     const int s = t % STAGES;
+    const int kg = (kt0 + t) * BK;  // global K coordinate
     uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
     uint8_t* sb = sa + Cfg::A_BYTES;
     mbar_arrive_expect_tx(&full[s], Cfg::TX_BYTES);
-    if (A_MN) tma_load_3d(sa, &tmap_a, &full[s], m0, t * BK, z);
-    else      tma_load_3d(sa, &tmap_a, &full[s], t * BK, m0, z);
-    if (B_MN) tma_load_3d(sb, &tmap_b, &full[s], n0, t * BK, z);
-    else      tma_load_3d(sb, &tmap_b, &full[s], t * BK, n0, z);
+    if (A_MN) tma_load_3d(sa, &tmap_a, &full[s], m0, kg, z);
+    else      tma_load_3d(sa, &tmap_a, &full[s], kg, m0, z);
+    if (B_MN) tma_load_3d(sb, &tmap_b, &full[s], n0, kg, z);
+    else      tma_load_3d(sb, &tmap_b, &full[s], kg, n0, z);
   };
   if (tid == 0) {
     for (int t = 0; t < STAGES && t < ktiles; ++t) issue(t);
@@ -197,7 +217,7 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
       }
       __syncthreads();
     }
-    const int kcur = min(k_total - kt * BK, BK);
+    const int kcur = min(k_total - (kt0 + kt) * BK, BK);
 
     auto step = [&](const float (&af)[TM], const float (&bf)[TN]) {
       if constexpr (PN) outer_ffma2_n<TM, TN>(acc2, af, bf);
@@ -275,6 +295,45 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  if constexpr (KS > 1) {
+    // ---- split-K: ranks 1.. park their partials, rank 0 adds them in order ----
+    // Every stage this CTA loaded has been consumed, so the ring is free.
+    constexpr int NACC = (PN ? TM : TM / 2) * (PN ? TN / 2 : TN);  // float2 per thread
+    float2* park = reinterpret_cast<float2*>(smem) + static_cast<size_t>(tid) * NACC;
+    __syncthreads();  // every warp is done reading the ring
+    if (krank != 0) {
+#pragma unroll
+      for (int i = 0; i < (PN ? TM : TM / 2); ++i)
+#pragma unroll
+        for (int j = 0; j < (PN ? TN / 2 : TN); ++j) park[i * (PN ? TN / 2 : TN) + j] = acc2[i][j];
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (krank == 0) {
+      const uint32_t park_s = smem_u32(park);
+#pragma unroll
+      for (int q = 1; q < KS; ++q) {
+        uint32_t remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(park_s), "r"(q));
+#pragma unroll
+        for (int i = 0; i < (PN ? TM : TM / 2); ++i)
+#pragma unroll
+          for (int j = 0; j < (PN ? TN / 2 : TN); j += 2) {
+            float4 v;
+            asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+                         : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                         : "r"(remote + static_cast<uint32_t>((i * (PN ? TN / 2 : TN) + j) * 8)));
+            acc2[i][j].x = __fadd_rn(acc2[i][j].x, v.x);
+            acc2[i][j].y = __fadd_rn(acc2[i][j].y, v.y);
+            acc2[i][j + 1].x = __fadd_rn(acc2[i][j + 1].x, v.z);
+            acc2[i][j + 1].y = __fadd_rn(acc2[i][j + 1].y, v.w);
+          }
+      }
+    }
+    // peers keep their shared memory until rank 0 has read it
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (krank != 0) return;
   }
 
   // ---- epilogue (reference order: alpha*acc, then + beta*C) ----

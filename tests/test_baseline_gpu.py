@@ -5,8 +5,10 @@ and (4096,128,9216), C4 256-instance prefixes of 32^3 / 64^3; S and H):
 * the public routine on the GPU is within 2x the reference tolerance of the
   REFERENCE's own output (test_level3.py:84-85's pairwise rule) and within
   1x of the float64 product;
-* SGEMM equals the sequential-k C oracle bitwise on every row of sampled
-  rows (all rows for the batched prefixes) unless the route split K;
+* SGEMM equals the sequential-k C oracle bitwise on sampled rows (all rows
+  for the batched prefixes); where the route splits K (kernel name
+  ..._splitkN) the oracle's chain is cut at the same rank boundaries and
+  summed in rank order (oracle.seqk_gemm_split);
 * the kernel that served the call is the one bench.py reports for that
   config (so the benchmarked kernel is the tested kernel).
 Plus the routes no golden reaches: the 128x64 TMA SGEMM at 1024^3/1536^3 in
@@ -32,7 +34,7 @@ R, N, Tr = Layout.ROW_MAJOR, Transpose.NO, Transpose.YES
 EXPECTED_KERNEL = {
     "C1_S": "sgemm_tma_128x64",
     "C3a_S": "sgemm_tma_64x32",
-    "C3b_S": "sgemm_tma_64x32",
+    "C3b_S": "sgemm_tma_128x64",
     "C1_H": "hgemm_tc_tma_128x64",
     "C3a_H": "hgemm_tc_tma_128x64",
     "C3b_H": "hgemm_tc_splitk",
@@ -59,6 +61,24 @@ def gpu_tolerance(prec, a, b, rows=64):
     if prec == "H":
         tol = tol + 2.0 ** -11 * wide.abs() + 2.0 ** -24
     return tol + 1e-30, wide
+
+
+def split_of(kernel: str) -> int:
+    """The split-K factor a SGEMM route used (1 when K was not split)."""
+    import re
+
+    m = re.search(r"_splitk(\d+)", kernel)
+    return int(m.group(1)) if m else 1
+
+
+def seq_rows(kernel, rows, n, k, a_rows, b, out):
+    """Row-major NN oracle for the route that ran: the sequential-k chain, or
+    the same chain cut at the split-K rank boundaries (oracle.seqk_gemm_split)."""
+    ks = split_of(kernel)
+    if ks == 1:
+        orc.seqk_gemm("S", True, False, False, rows, n, k, 1.0, a_rows, 0, k, b, 0, n, 0.0, out, 0, n)
+    else:
+        orc.seqk_gemm_split("S", True, False, False, rows, n, k, 1.0, a_rows, 0, k, b, 0, n, 0.0, out, 0, n, ks)
 
 
 def run_case(ctx, case):
@@ -95,15 +115,14 @@ def test_baseline_config_parity(ctx, case):
     r_wide = float(((got - wide).abs() / tol).max())
     assert r_ref <= 2.0, f"vs reference output: {r_ref:.3f} x tol ({kernel})"
     assert r_wide <= 1.0, f"vs float64 product: {r_wide:.3f} x tol ({kernel})"
-    if case["prec"] == "S" and "splitk" not in kernel:
+    if case["prec"] == "S":
         # sequential-k chain, bitwise: sampled rows (every row of the prefix batches)
         c_host = ct.cpu().numpy()
         if case["kind"] == "gemm":
             rows = np.sort(np.random.default_rng(3).choice(m, min(m, 48), replace=False))
             sub_a = np.ascontiguousarray(a.reshape(m, k)[rows]).reshape(-1)
             sub = np.zeros(len(rows) * n, np.float32)
-            orc.seqk_gemm("S", True, False, False, len(rows), n, k, 1.0, sub_a, 0, k, b, 0, n, 0.0,
-                          sub, 0, n)
+            seq_rows(kernel, len(rows), n, k, sub_a, b, sub)
             assert sub.tobytes() == np.ascontiguousarray(c_host.reshape(m, n)[rows]).tobytes()
         else:
             seq = np.zeros(m * n * batch, np.float32)
@@ -115,9 +134,10 @@ def test_baseline_config_parity(ctx, case):
 @pytest.mark.parametrize("size", [1024, 1536])
 @pytest.mark.parametrize("ta,tbn", [("n", "n"), ("t", "n"), ("t", "t")])
 def test_sgemm_128x64_route(ctx, size, ta, tbn):
-    """The 128x64 TMA SGEMM (the kernel serving C1) in each layout it takes
-    (row-major: op(B) N-contiguous or op(A) M-contiguous, i.e. every (ta, tb)
-    but (N, T)): bitwise against the sequential-k oracle on sampled rows."""
+    """The 128x64 TMA SGEMM (the kernel serving C1; 1024^3 takes its split-K
+    variant) in each layout it takes (row-major: op(B) N-contiguous or op(A)
+    M-contiguous, i.e. every (ta, tb) but (N, T)): bitwise against the
+    sequential-k oracle (split at the same K boundaries) on sampled rows."""
     import torch
 
     m = n = k = size
@@ -138,8 +158,7 @@ def test_sgemm_128x64_route(ctx, size, ta, tbn):
     rows = np.sort(np.random.default_rng(size).choice(m, 40, replace=False))
     sub_a = np.ascontiguousarray(A[rows]).reshape(-1)
     sub = np.zeros(len(rows) * n, np.float32)
-    orc.seqk_gemm("S", True, False, False, len(rows), n, k, 1.0, sub_a, 0, k,
-                  np.ascontiguousarray(B).reshape(-1), 0, n, 0.0, sub, 0, n)
+    seq_rows(kernel, len(rows), n, k, sub_a, np.ascontiguousarray(B).reshape(-1), sub)
     assert sub.tobytes() == np.ascontiguousarray(got[rows]).tobytes()
 
 

@@ -197,3 +197,32 @@ def test_known_answers():
     c0 = np.array([7.0], np.float32)
     orc.seqk_gemm("S", False, False, False, 0, 0, 0, 1.0, c0, 0, 1, c0, 0, 1, 0.0, c0, 0, 1)
     assert c0.tolist() == [7.0]
+
+
+def test_seqk_split_oracle():
+    """oracle.seqk_gemm_split: KS = 1 is the sequential-k chain bitwise; a
+    split is the rank-order sum of the chains over the K ranges, within the
+    reference tolerance of the float64 product."""
+    rng = np.random.default_rng(9)
+    m, n, k = 7, 9, 300
+    a = rng.uniform(-1, 1, m * k).astype(np.float32)
+    b = rng.uniform(-1, 1, k * n).astype(np.float32)
+    one = np.zeros(m * n, np.float32)
+    orc.seqk_gemm_split("S", True, False, False, m, n, k, 1.5, a, 0, k, b, 0, n, 0.0, one, 0, n, 1)
+    seq = np.zeros(m * n, np.float32)
+    orc.seqk_gemm("S", True, False, False, m, n, k, 1.5, a, 0, k, b, 0, n, 0.0, seq, 0, n)
+    assert one.tobytes() == seq.tobytes()
+    A, B = a.reshape(m, k), b.reshape(k, n)
+    want = 1.5 * (A.astype(np.float64) @ B.astype(np.float64))
+    for ks in (2, 4):
+        got = np.zeros(m * n, np.float32)
+        orc.seqk_gemm_split("S", True, False, False, m, n, k, 1.5, a, 0, k, b, 0, n, 0.0, got, 0, n, ks)
+        # manual: chains over [0,160) / [160,300) for ks=2 (5 stages of 32 per rank)
+        assert orc.allclose_tol(got.reshape(m, n), want, 1.5 * orc.gemm_tolerance(A, B, "S"))
+    p0 = np.zeros(m * n, np.float32)
+    p1 = np.zeros(m * n, np.float32)
+    orc.seqk_gemm("S", True, False, False, m, n, 160, 1.0, a, 0, k, b, 0, n, 0.0, p0, 0, n)
+    orc.seqk_gemm("S", True, False, False, m, n, 140, 1.0, a, 160, k, b, 160 * n, n, 0.0, p1, 0, n)
+    two = np.zeros(m * n, np.float32)
+    orc.seqk_gemm_split("S", True, False, False, m, n, k, 1.0, a, 0, k, b, 0, n, 0.0, two, 0, n, 2)
+    assert two.tobytes() == (p0 + p1).astype(np.float32).tobytes()
