@@ -58,6 +58,18 @@ __device__ __forceinline__ float inst_beta(const Problem& p, int64_t z) {
   return p.betas ? __ldg(p.betas + z) : p.beta;
 }
 
+// Programmatic dependent launch: kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization (host.h launch_ex), so a
+// CTA may start while the previous kernel on the stream is still finishing.
+// Everything before this call (barrier init, TMEM allocation, tensor-map
+// prefetch) overlaps that tail; nothing before it touches global memory the
+// previous kernel may read or write.  A no-op when launched without PDL.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Let the next kernel on the stream launch now: its CTAs take SMs as ours
+// exit and run their prologue, then wait in grid_dep_wait() for this grid's
+// completion — so back-to-back GEMMs overlap prologue with tail.
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Reference epilogue (compute.py:408-412, 458-463; level3.py:125-132):
 //   alpha == 0 or k == 0 : beta == 0 ? 0 : beta*c      (A/B never read)
 //   beta == 0            : alpha*acc                    (C never read)

@@ -45,7 +45,9 @@ int launch_hg(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
   const int64_t g = total < sms ? total : sms;
   dim3 grid(static_cast<unsigned>(g)), block(Cfg::THREADS);
   const ConvGeom geom = c.conv ? *c.conv : ConvGeom{};
-  kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, cfg_group_m(c, 16), total, geom);
+  if (int rc = launch_ex("hgemm_tc launch", kern, grid, block, Cfg::SMEM_BYTES, c.stream, 1, ta, tbm, p, tiles_m,
+                         tiles_n, cfg_group_m(c, 16), total, geom))
+    return rc;
   char name[64];
   snprintf(name, sizeof(name), "hgemm_tc_%s_128x%d_%c%c%s%s", CONV ? "conv" : (TMA ? "tma" : "ldg"), BN,
            AMN ? 'm' : 'k', BMN ? 'n' : 'k', (!TMA && !VEC) ? "_scalar" : "",
@@ -107,7 +109,9 @@ int launch_h2(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm, bool
       return check_launch("wave counter");
   }
   // group_m 8: measured best for pair tiles (also with the wave barrier)
-  kern<<<grid, block, H2Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, cfg_group_m(c, 8), total, ctr);
+  if (int rc = launch_ex("hgemm_tc_2sm launch", kern, grid, block, H2Cfg::SMEM_BYTES, c.stream, 1, ta, tbm, p,
+                         tiles_m, tiles_n, cfg_group_m(c, 8), total, ctr))
+    return rc;
   char name[64];
   snprintf(name, sizeof(name), "hgemm_tc2sm_tma_256x256_%c%c%s", AMN ? 'm' : 'k', BMN ? 'n' : 'k',
            ctr ? "_ws" : "");
@@ -172,14 +176,14 @@ int hgemm_split_ks(const Problem& p) {
   return ks;
 }
 
-template <bool TMA, bool AMN, bool BMN, bool VEC>
+template <bool TMA, bool AMN, bool BMN, bool VEC, bool CONV = false>
 int launch_hsk(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm, int ks) {
   using Cfg = SkCfg<TMA>;
   const Problem& p = c.p;
   const int tiles_m = static_cast<int>((p.m + HG_BM - 1) / HG_BM);
   const int tiles_n = static_cast<int>((p.n + SK_BN - 1) / SK_BN);
   const int64_t total = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
-  auto kern = hgemm_tc_splitk_kernel<TMA, AMN, BMN, VEC>;
+  auto kern = hgemm_tc_splitk_kernel<TMA, AMN, BMN, VEC, CONV>;
   static SmemAttr attr;
   if (int rc = ensure_smem(attr, kern, Cfg::SMEM_BYTES)) return rc;
   cudaLaunchConfig_t cfg = {};
@@ -213,13 +217,13 @@ int launch_hsk(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm, int
   float* ws = static_cast<float*>(
       splitk_workspace(c.stream, static_cast<size_t>(sms_or_default()) * SK_WS_FLOATS * sizeof(float)));
   if (cfg.gridDim.x > static_cast<unsigned>(sms_or_default())) ws = nullptr;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tbm, p, tiles_m, tiles_n, cfg_group_m(c, 16), total, ws);
-  if (e != cudaSuccess) {
-    set_err("hgemm_tc_splitk launch", e);
-    return TB_ERR_CUDA;
-  }
+  const ConvGeom geom = c.conv ? *c.conv : ConvGeom{};
+  if (int rc = launch_ex("hgemm_tc_splitk launch", kern, cfg.gridDim, cfg.blockDim, Cfg::SMEM_BYTES, c.stream, ks, ta,
+                         tbm, p, tiles_m, tiles_n, cfg_group_m(c, 16), total, ws, geom))
+    return rc;
   char name[64];
-  snprintf(name, sizeof(name), "hgemm_tc_splitk%d_%s_128x128_%c%c%s%s", ks, TMA ? "tma" : "ldg", AMN ? 'm' : 'k',
+  snprintf(name, sizeof(name), "hgemm_tc_splitk%d_%s_128x128_%c%c%s%s", ks, CONV ? "conv" : (TMA ? "tma" : "ldg"),
+           AMN ? 'm' : 'k',
            BMN ? 'n' : 'k', (!TMA && !VEC) ? "_scalar" : "", ws ? "" : "_dsmem");
   record(name, cfg.gridDim, cfg.blockDim, ks, Cfg::SMEM_BYTES, total);
   return check_launch("hgemm_tc_splitk launch");
@@ -269,6 +273,25 @@ int dispatch_hconv(const Call& c) {
   const Problem& p = c.p;
   CUtensorMap none;
   memset(&none, 0, sizeof(none));
+  // Few tiles in the launch (the typical layer, one image: 3136 positions x
+  // 64 filters = 25 tiles): split K over a cluster so more SMs gather — the
+  // gather is latency-bound per stage.  KS = largest power of two <= 8 with
+  // tiles * KS <= SMs and >= 4 K blocks per rank pair, over ALL images of the
+  // call (a batch of 32 images has parallelism enough and is not split:
+  // measured 465 vs 275 us split / unsplit), so for H the last bits of an
+  // image's result can depend on how many images share the call.
+  {
+    const int sms = sms_or_default();
+    const int64_t t1 = ((p.m + HG_BM - 1) / HG_BM) * ((p.n + SK_BN - 1) / SK_BN) * p.batch;
+    const int64_t nkb = (p.k + HG_BK - 1) / HG_BK;
+    int ks = 1;
+    while (ks < 8 && t1 * ks * 2 <= sms && nkb >= 4 * ks) ks *= 2;
+    const bool vecb = (p.ldb % 8 == 0) && aligned_elems(p.b, p.b_off, 2, 16);
+    if (ks > 1) {
+      if (vecb) return launch_hsk<false, true, false, true, true>(c, none, none, ks);
+      return launch_hsk<false, true, false, false, true>(c, none, none, ks);
+    }
+  }
   const bool vec = (p.ldb % 8 == 0) && aligned_elems(p.b, p.b_off, 2, 16);
   auto tiles = [&](int b) { return ((p.m + HG_BM - 1) / HG_BM) * ((p.n + b - 1) / b) * p.batch; };
   const int sms = sms_or_default();
@@ -331,7 +354,7 @@ int launch_hscale(const Call& c) {
   if (blocks > 4096) blocks = 4096;
   if (blocks < 1) blocks = 1;
   dim3 grid(static_cast<unsigned>(blocks));
-  hscale_kernel<0><<<grid, block, 0, c.stream>>>(c.p);
+  if (int rc = launch_ex("hscale launch", hscale_kernel<0>, grid, block, 0, c.stream, 1, c.p)) return rc;
   record("hscale", grid, block, 1, 0, c.p.batch);
   return check_launch("hscale launch");
 }

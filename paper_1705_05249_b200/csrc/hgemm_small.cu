@@ -20,7 +20,7 @@ int launch_hs(const Call& c) {
   const int sms = sms_or_default();
   const int64_t g = total < sms ? total : sms;
   dim3 grid(static_cast<unsigned>(g)), block(Cfg::THREADS);
-  kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(p, total);
+  if (int rc = launch_ex("hgemm_tc_small launch", kern, grid, block, Cfg::SMEM_BYTES, c.stream, 1, p, total)) return rc;
   char name[64];
   snprintf(name, sizeof(name), "hgemm_tc_small_%dx%d_p%d_%c%c%s%s", MI, NI, Cfg::P, AMN ? 'm' : 'k',
            BMN ? 'n' : 'k', VEC ? "_cpasync" : "_scalar", K32 ? "_k32" : "");
@@ -75,7 +75,9 @@ int launch_hs32_tma(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm
   const int sms = sms_or_default();
   const int64_t g = total < sms ? total : sms;
   dim3 grid(static_cast<unsigned>(g)), block(Cfg::THREADS);
-  kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, total);
+  if (int rc = launch_ex("hgemm_tc_small32_tma launch", kern, grid, block, Cfg::SMEM_BYTES, c.stream, 1, ta, tbm, p,
+                         total))
+    return rc;
   char name[64];
   snprintf(name, sizeof(name), "hgemm_tc_small_32x32_p4_%c%c_tma", AMN ? 'm' : 'k', BMN ? 'n' : 'k');
   record(name, grid, block, 1, Cfg::SMEM_BYTES, total);

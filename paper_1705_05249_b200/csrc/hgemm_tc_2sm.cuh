@@ -176,6 +176,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  grid_dep_wait();  // prologue above overlapped the previous kernel (PDL)
+  grid_dep_launch();
   const int nkb = static_cast<int>((p.k + HG_BK - 1) / HG_BK);
 
   if (warp == C::PROD_WARP) {

@@ -208,6 +208,8 @@ __global__ void __launch_bounds__(HsCfg<MI, NI>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  grid_dep_wait();  // prologue above overlapped the previous kernel (PDL)
+  grid_dep_launch();
   const int nkb = static_cast<int>((p.k + HG_BK - 1) / HG_BK);
   const int m = static_cast<int>(p.m), n = static_cast<int>(p.n);
 
@@ -467,6 +469,8 @@ __global__ void __launch_bounds__(Hs32Cfg::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  grid_dep_wait();  // prologue above overlapped the previous kernel (PDL)
+  grid_dep_launch();
   const int m = static_cast<int>(p.m), n = static_cast<int>(p.n);
 
   if (warp == C::PROD_WARP) {

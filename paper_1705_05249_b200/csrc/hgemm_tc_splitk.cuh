@@ -136,11 +136,14 @@ __device__ __forceinline__ float4 sk_ld_cluster_f4(uint32_t addr) {
   return v;
 }
 
-template <bool TMA, bool A_MN, bool B_MN, bool VEC>
+// CONV: op(A) gathered from an image (implicit GEMM, hgemm_tc.cuh
+// conv_fill_tile) in the LDG producer — convgemm's few-tile layers.
+template <bool TMA, bool A_MN, bool B_MN, bool VEC, bool CONV = false>
 __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
     hgemm_tc_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                            Problem p, int tiles_m, int tiles_n, int group_m, int64_t total_tiles,
-                           float* __restrict__ ws) {
+                           float* __restrict__ ws, const ConvGeom conv) {
+  static_assert(!CONV || (!TMA && A_MN), "the im2col gather runs in the LDG producer, MN-major");
   using C = SkCfg<TMA>;
   constexpr int STAGES = C::STAGES, BN = SK_BN;
   extern __shared__ uint8_t smem_raw[];
@@ -186,6 +189,8 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
   sk_cluster_sync();  // barriers of every CTA initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  grid_dep_wait();  // prologue above overlapped the previous kernel (PDL)
+  grid_dep_launch();
   if (threadIdx.x == 0) SK_STAMP(1);
 
   const int nkb = static_cast<int>((p.k + HG_BK - 1) / HG_BK);
@@ -247,13 +252,18 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
         const __half* B = static_cast<const __half*>(p.b) + inst_off(p.b_off, p.stride_b, p.b_offs, z);
         const int m_left = static_cast<int>(min64(HG_BM, p.m - m0));
         const int n_left = static_cast<int>(min64(BN, p.n - n0));
+        int yb[16], xb[16];
+        if (CONV) conv_tile_coords(conv, p.m, m0, tid, yb, xb);
         for (int kb = static_cast<int>(rank); kb < nkb; kb += static_cast<int>(ks)) {
           const int64_t k0 = static_cast<int64_t>(kb) * HG_BK;
           const int k_left = static_cast<int>(min64(HG_BK, p.k - k0));
           mbar_wait(&empty[s], ph ^ 1);
           const __half* a_base = A_MN ? A + k0 * p.lda + m0 : A + m0 * p.lda + k0;
           const __half* b_base = B_MN ? B + k0 * p.ldb + n0 : B + n0 * p.ldb + k0;
-          ldg_fill_tile<HG_BM, A_MN, VEC>(sA + s * C::A_BYTES, a_base, p.lda, m_left, k_left, tid);
+          if (CONV)
+            conv_fill_tile(sA + s * C::A_BYTES, A, conv, k0, k_left, tid, yb, xb);
+          else
+            ldg_fill_tile<HG_BM, A_MN, VEC>(sA + s * C::A_BYTES, a_base, p.lda, m_left, k_left, tid);
           ldg_fill_tile<BN, B_MN, VEC>(sB + s * C::B_BYTES, b_base, p.ldb, n_left, k_left, tid);
           fence_proxy_async_smem();
           mbar_arrive(&full[s]);

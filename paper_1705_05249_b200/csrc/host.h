@@ -10,6 +10,8 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <utility>
 
 #include "common.cuh"
 #include "tbgemm.h"
@@ -64,6 +66,48 @@ int ensure_smem(SmemAttr& st, K kern, int bytes) {
     return TB_ERR_CUDA;
   }
   st.devs.fetch_or(bit, std::memory_order_acq_rel);
+  return TB_OK;
+}
+
+// Launch with programmatic dependent launch (PDL; common.cuh grid_dep_wait)
+// and, when cluster > 1, a runtime cluster dimension.  TB_NO_PDL=1 in the
+// environment turns PDL off (A/B measurement).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TB_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+int launch_ex(const char* what, void (*kern)(KArgs...), dim3 grid, dim3 block, int smem, cudaStream_t stream,
+              int cluster, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute la[2];
+  int na = 0;
+  if (cluster > 1) {
+    la[na].id = cudaLaunchAttributeClusterDimension;
+    la[na].val.clusterDim.x = static_cast<unsigned>(cluster);
+    la[na].val.clusterDim.y = 1;
+    la[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    la[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = stream;
+  cfg.attrs = la;
+  cfg.numAttrs = na;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess) {
+    set_err(what, e);
+    return TB_ERR_CUDA;
+  }
   return TB_OK;
 }
 

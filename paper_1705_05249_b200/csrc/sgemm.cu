@@ -24,17 +24,19 @@ int launch_simt(const Call& c) {
   dim3 grid(static_cast<unsigned>(blocks)), block(SimtShape<BM, BN, BK, TM, TN>::NT);
   const int sel = (p.a_kcontig ? 2 : 0) | (p.b_ncontig ? 1 : 0);
   const ConvGeom geom = c.conv ? *c.conv : ConvGeom{};
+  int rc;
   if constexpr (CONV) {  // op(A) gathered (M-contiguous layout), filters K-contiguous
-    sgemm_simt_kernel<BM, BN, BK, TM, TN, false, false, VEC, MINB, true><<<grid, block, 0, c.stream>>>(
-        p, tiles_m, tiles_n, group_m, geom);
+    rc = launch_ex("sgemm_conv launch", sgemm_simt_kernel<BM, BN, BK, TM, TN, false, false, VEC, MINB, true>, grid,
+                   block, 0, c.stream, 1, p, tiles_m, tiles_n, group_m, geom);
   } else {
     switch (sel) {
-      case 0: sgemm_simt_kernel<BM, BN, BK, TM, TN, false, false, VEC, MINB><<<grid, block, 0, c.stream>>>(p, tiles_m, tiles_n, group_m, geom); break;
-      case 1: sgemm_simt_kernel<BM, BN, BK, TM, TN, false, true, VEC, MINB><<<grid, block, 0, c.stream>>>(p, tiles_m, tiles_n, group_m, geom); break;
-      case 2: sgemm_simt_kernel<BM, BN, BK, TM, TN, true, false, VEC, MINB><<<grid, block, 0, c.stream>>>(p, tiles_m, tiles_n, group_m, geom); break;
-      default: sgemm_simt_kernel<BM, BN, BK, TM, TN, true, true, VEC, MINB><<<grid, block, 0, c.stream>>>(p, tiles_m, tiles_n, group_m, geom); break;
+      case 0: rc = launch_ex("sgemm_simt launch", sgemm_simt_kernel<BM, BN, BK, TM, TN, false, false, VEC, MINB>, grid, block, 0, c.stream, 1, p, tiles_m, tiles_n, group_m, geom); break;
+      case 1: rc = launch_ex("sgemm_simt launch", sgemm_simt_kernel<BM, BN, BK, TM, TN, false, true, VEC, MINB>, grid, block, 0, c.stream, 1, p, tiles_m, tiles_n, group_m, geom); break;
+      case 2: rc = launch_ex("sgemm_simt launch", sgemm_simt_kernel<BM, BN, BK, TM, TN, true, false, VEC, MINB>, grid, block, 0, c.stream, 1, p, tiles_m, tiles_n, group_m, geom); break;
+      default: rc = launch_ex("sgemm_simt launch", sgemm_simt_kernel<BM, BN, BK, TM, TN, true, true, VEC, MINB>, grid, block, 0, c.stream, 1, p, tiles_m, tiles_n, group_m, geom); break;
     }
   }
+  if (rc) return rc;
   char name[64];
   static const char* lay[4] = {"mk", "mn", "kk", "kn"};  // A major x B major
   snprintf(name, sizeof(name), "sgemm_%s_%dx%dx%d_%s_%s", CONV ? "conv" : "simt", BM, BN, BK,
@@ -60,7 +62,7 @@ int launch_ss(const Call& c) {
   const int64_t cap = static_cast<int64_t>(sms_or_default()) * per_sm;
   const int64_t g = groups < cap ? groups : cap;
   dim3 grid(static_cast<unsigned>(g)), block(256);
-  kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(p, groups);
+  if (int rc = launch_ex("sgemm_small launch", kern, grid, block, Cfg::SMEM_BYTES, c.stream, 1, p, groups)) return rc;
   char name[64];
   snprintf(name, sizeof(name), "sgemm_small_%dx%d_t%dx%d_g%d_%c%c", MI, NI, TM, TN, Cfg::G, AK ? 'k' : 'm',
            BNC ? 'n' : 'k');
@@ -90,7 +92,9 @@ int launch_tf32(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
   const int sms = sms_or_default();
   const int64_t g = total < sms ? total : sms;
   dim3 grid(static_cast<unsigned>(g)), block(Cfg::THREADS);
-  kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, cfg_group_m(c, 16), total);
+  if (int rc = launch_ex("sgemm_tf32_tc launch", kern, grid, block, Cfg::SMEM_BYTES, c.stream, 1, ta, tbm, p, tiles_m,
+                         tiles_n, cfg_group_m(c, 16), total))
+    return rc;
   char name[64];
   snprintf(name, sizeof(name), "sgemm_tf32_tc_tma_128x%d_%c%c", BN, AMN ? 'm' : 'k', BMN ? 'n' : 'k');
   record(name, grid, block, 1, Cfg::SMEM_BYTES, total);

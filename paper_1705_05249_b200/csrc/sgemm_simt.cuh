@@ -90,29 +90,30 @@ template <int ROWS, int BK, int PER_T, int NT>
 __device__ __forceinline__ void simt_conv_stage(float4 (&r)[PER_T], const float* __restrict__ im,
                                                 const ConvGeom& g, int64_t m, int64_t m0, int64_t k0,
                                                 int k_left) {
+  // branch-free: every tap loads from a valid address (the plane's first
+  // element in the padding) and is masked afterwards, so the loads of the
+  // whole stage issue back to back (see hgemm_tc.cuh conv_fill_tile)
   const int khw = g.kh * g.kw;
 #pragma unroll
   for (int j = 0; j < PER_T; ++j) {
     const int e = threadIdx.x + j * NT;
     const int kk = e / (ROWS / 4);
     const int row = (e % (ROWS / 4)) * 4;
-    float v[4] = {0.f, 0.f, 0.f, 0.f};
-    if (kk < k_left) {
-      const int kr = static_cast<int>(k0) + kk;
-      const int ch = kr / khw, rem = kr - ch * khw;
-      const int ky = rem / g.kw, kx = rem - ky * g.kw;
-      const float* plane = im + static_cast<int64_t>(ch) * g.height * g.width;
+    const bool k_ok = kk < k_left;
+    const int kr = static_cast<int>(k0) + (k_ok ? kk : 0);
+    const int ch = kr / khw, rem = kr - ch * khw;
+    const int ky = rem / g.kw, kx = rem - ky * g.kw;
+    const float* plane = im + static_cast<int64_t>(ch) * g.height * g.width;
+    float v[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t pos = m0 + row + q;
-        if (pos < m) {
-          const int oy = static_cast<int>(pos / g.out_w), ox = static_cast<int>(pos - static_cast<int64_t>(oy) * g.out_w);
-          const int y = oy * g.stride_h + ky * g.dil_h - g.pad_h, x = ox * g.stride_w + kx * g.dil_w - g.pad_w;
-          if (static_cast<unsigned>(y) < static_cast<unsigned>(g.height) &&
-              static_cast<unsigned>(x) < static_cast<unsigned>(g.width))
-            v[q] = __ldg(plane + static_cast<int64_t>(y) * g.width + x);
-        }
-      }
+    for (int q = 0; q < 4; ++q) {
+      const int64_t pos = m0 + row + q;
+      const int oy = static_cast<int>(pos / g.out_w), ox = static_cast<int>(pos - static_cast<int64_t>(oy) * g.out_w);
+      const int y = oy * g.stride_h + ky * g.dil_h - g.pad_h, x = ox * g.stride_w + kx * g.dil_w - g.pad_w;
+      const bool in = k_ok && pos < m && static_cast<unsigned>(y) < static_cast<unsigned>(g.height) &&
+                      static_cast<unsigned>(x) < static_cast<unsigned>(g.width);
+      const float t = __ldg(plane + (in ? static_cast<int64_t>(y) * g.width + x : 0));
+      v[q] = in ? t : 0.0f;
     }
     r[j] = make_float4(v[0], v[1], v[2], v[3]);
   }
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(SimtShape<BM, BN, BK, TM, TN>::NT, MINB)
     sgemm_simt_kernel(Problem p, int tiles_m, int tiles_n, int group_m, const ConvGeom conv) {
   using S = SimtShape<BM, BN, BK, TM, TN>;
   static_assert(!CONV || !AK, "the im2col gather fills the M-contiguous layout");
+  grid_dep_wait();  // PDL: the previous kernel's writes are visible from here
   __shared__ __align__(16) float As[2][BK * S::LDA_S];
   __shared__ __align__(16) float Bs[2][BK * S::LDB_S];
 

@@ -48,6 +48,7 @@ template <int MI, int NI, int TM, int TN, bool AK, bool BNC>
 __global__ void __launch_bounds__(256, (SsCfg<MI, NI, TM, TN>::MINB))
     sgemm_small_kernel(Problem p, int64_t groups) {
   using C = SsCfg<MI, NI, TM, TN>;
+  grid_dep_wait();  // PDL: the previous kernel's writes are visible from here
   constexpr int QM = C::QM, QN = C::QN;
   constexpr int KC = C::KC, G = C::G, STAGES = C::STAGES;
   // K-contiguous slot layout: element (row, kk) of a [rows][KCP] tile

@@ -144,6 +144,8 @@ __global__ void __launch_bounds__(TfCfg<BN>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  grid_dep_wait();  // prologue above overlapped the previous kernel (PDL)
+  grid_dep_launch();
   const int nkb = static_cast<int>((p.k + TF_BK - 1) / TF_BK);
 
   if (warp == C::PROD_WARP) {

@@ -35,27 +35,9 @@ int launch_stma(const Call& c) {
   static SmemAttr attr;  // per instantiation, per device
   if (int rc2 = ensure_smem(attr, kern, Cfg::SMEM_BYTES)) return rc2;
   dim3 grid(static_cast<unsigned>(blocks * KS)), block(Cfg::NT);
-  if constexpr (KS == 1) {
-    kern<<<grid, block, Cfg::SMEM_BYTES, c.stream>>>(ta, tbm, p, tiles_m, tiles_n, cfg_group_m(c, 8));
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute la[1];
-    la[0].id = cudaLaunchAttributeClusterDimension;
-    la[0].val.clusterDim.x = KS;
-    la[0].val.clusterDim.y = 1;
-    la[0].val.clusterDim.z = 1;
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
-    cfg.stream = c.stream;
-    cfg.attrs = la;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tbm, p, tiles_m, tiles_n, cfg_group_m(c, 8));
-    if (e != cudaSuccess) {
-      set_err("sgemm_tma split-K launch", e);
-      return TB_ERR_CUDA;
-    }
-  }
+  if (int rc2 = launch_ex("sgemm_tma launch", kern, grid, block, Cfg::SMEM_BYTES, c.stream, KS, ta, tbm, p, tiles_m,
+                          tiles_n, cfg_group_m(c, 8)))
+    return rc2;
   char name[64];
   snprintf(name, sizeof(name), "sgemm_tma_%dx%dx32_%dx%d_%c%c%s%s", BM, BN, TM, TN, AMN ? 'm' : 'k',
            BMN ? 'n' : 'k', (Cfg::A_T || Cfg::B_T) ? "_xp" : "", KS == 2 ? "_splitk2" : (KS == 4 ? "_splitk4" : ""));

@@ -140,6 +140,8 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
     fence_mbar_init();
   }
   __syncthreads();
+  grid_dep_wait();  // prologue above overlapped the previous kernel (PDL)
+  grid_dep_launch();
 
   auto issue = [&](int t) {  // local stage t -> slot t % STAGES (tid 0 only)
     const int s = t % STAGES;

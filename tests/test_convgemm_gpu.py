@@ -7,7 +7,8 @@ convolution):
   followed by a GEMM: S bitwise equal to the sequential-k C oracle on the
   golden column matrix; H within the FP16 tolerance of the float64 product;
 * against this library's own ``im2col`` + ``gemm`` (bitwise, both precisions:
-  the same per-element arithmetic);
+  the same per-element arithmetic — except few-tile H layers, which split K
+  over a cluster and are checked within the FP16 tolerance);
 * batched images, offsets, sentinel regions around the result untouched.
 """
 
@@ -100,6 +101,7 @@ def test_convgemm_equals_im2col_plus_gemm(ctx, prec, geom):
     res = tb.buffer_alloc(ctx, prec, r_off + batch * nk * cols)
     tb.convgemm(ctx, c, h, w_, kh, kw, ph, pw, sh, sw, dh, dw, nk, batch, im, kern, res,
                 im_offset=im_off, kernel_offset=k_off, result_offset=r_off)
+    conv_kernel = ctx.last_launch.native["kernel"]
     fused = res.device_tensor().clone()
     col = tb.buffer_alloc(ctx, prec, rows * cols)
     ref = tb.buffer_alloc(ctx, prec, r_off + batch * nk * cols)
@@ -110,7 +112,20 @@ def test_convgemm_equals_im2col_plus_gemm(ctx, prec, geom):
         tb.gemm(ctx, Layout.ROW_MAJOR, Transpose.NO, Transpose.YES, nk, cols, rows, 1.0, kern, col, 0.0, ref,
                 a_offset=k_off, lda=rows, ldb=rows, c_offset=r_off + b * nk * cols, ldc=cols)
     assert torch.equal(fused[:r_off], ref.device_tensor()[:r_off])
-    assert torch.equal(fused, ref.device_tensor()), ctx.last_launch.native["kernel"]
+    if "splitk" not in conv_kernel:
+        assert torch.equal(fused, ref.device_tensor()), conv_kernel
+    else:
+        # few-tile layers split K (a different summation order): within 2x
+        # the FP16 tolerance of the materialised result
+        W = kt[k_off:].view(nk, rows).double()
+        colm = col.device_tensor().view(cols, rows).t().double()   # last image's column matrix
+        want = W @ colm
+        tol = 4 * 2.0 ** -10 * rows * W.abs().amax(1, keepdim=True) * colm.abs().amax(0, keepdim=True) \
+            + 2.0 ** -11 * want.abs()
+        b = batch - 1
+        got = fused[r_off + b * nk * cols: r_off + (b + 1) * nk * cols].view(nk, cols).double()
+        mat = ref.device_tensor()[r_off + b * nk * cols: r_off + (b + 1) * nk * cols].view(nk, cols).double()
+        assert bool(((got - want).abs() <= tol).all()) and bool(((got - mat).abs() <= 2 * tol).all()), conv_kernel
 
 
 def test_convgemm_validation(ctx):
