@@ -333,7 +333,6 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
         uint32_t v[32];
         tmem_ld_32x32b_x32(t_row + cb * 32, v);
         tmem_ld_wait();
-#pragma unroll
         if (ws_mine != nullptr) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) __stcg(ws_mine + (cb * 32 + j) * SK_RED_LD + row, __uint_as_float(v[j]));

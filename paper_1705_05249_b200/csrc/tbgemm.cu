@@ -399,10 +399,34 @@ int tb_im2col(int prec, int64_t channels, int64_t height, int64_t width, int64_t
   g.stride_h = static_cast<int>(stride_h); g.stride_w = static_cast<int>(stride_w);
   g.dil_h = static_cast<int>(dilation_h); g.dil_w = static_cast<int>(dilation_w);
   g.out_h = static_cast<int>(out_h); g.out_w = static_cast<int>(out_w);
-  dim3 grid(static_cast<unsigned>((g.cols + IM2COL_TQ - 1) / IM2COL_TQ), static_cast<unsigned>(grid_y));
-  dim3 block(32, IM2COL_TY);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const char* name;
+  // patch-staged kernel (im2col.cuh) when its conditions hold; H only (S:
+  // 16.4 us against the tile kernel's 15.2 at the ResNet layer, L2 flushed)
+  if (prec == TB_PREC_H) {
+    const int es = prec == TB_PREC_S ? 4 : 2, vec = 16 / es, tr = 8 * vec;  // rows per CTA
+    const int kk = g.kh * g.kw;
+    // worst-case patch of 256 consecutive pixels x tr rows
+    const int64_t oy_span = 255 / g.out_w + 2;
+    const int64_t pr = (oy_span - 1) * g.stride_h + static_cast<int64_t>(g.kh - 1) * g.dil_h + 1;
+    const int64_t pw = static_cast<int64_t>(g.out_w - 1) * g.stride_w + static_cast<int64_t>(g.kw - 1) * g.dil_w + 1;
+    const int64_t nch = (tr - 1) / kk + 2;
+    const int64_t r_chunks = (g.rows + tr - 1) / tr, q_blocks = (g.cols + 255) / 256;
+    if (g.rows % vec == 0 && aligned_elems(col, col_off, es, 16) && nch * pr * pw * es <= IM2COL_PATCH_BYTES &&
+        pw <= 1024 && pr <= 1024 && r_chunks <= 65535 && q_blocks < 0x7fffffff) {
+      Im2colPatch pp;
+      pp.pw = static_cast<int>(pw);
+      pp.r_chunks = static_cast<int>(r_chunks);
+      const dim3 grid2(static_cast<unsigned>(q_blocks), static_cast<unsigned>(r_chunks)), block2(256);
+      im2col_vec_kernel<uint16_t><<<grid2, block2, 0, st>>>(static_cast<const uint16_t*>(im) + im_off,
+                                                            static_cast<uint16_t*>(col) + col_off, g, pp);
+      name = "im2col_vec_b16";
+      record(name, grid2, block2, 1, 0, g.rows * g.cols);
+      return check_launch("im2col launch");
+    }
+  }
+  dim3 grid(static_cast<unsigned>((g.cols + IM2COL_TQ - 1) / IM2COL_TQ), static_cast<unsigned>(grid_y));
+  dim3 block(32, IM2COL_TY);
   if (prec == TB_PREC_S) {
     im2col_kernel<uint32_t><<<grid, block, 0, st>>>(static_cast<const uint32_t*>(im) + im_off,
                                                       static_cast<uint32_t*>(col) + col_off, g);

@@ -41,7 +41,7 @@ def test_im2col_matches_reference_bitwise(ctx, i):
     assert rec.family == "transform" and rec.params == {"TDX": 16, "TDY": 16}
     assert rec.work_groups == (-(-cs["rows"] // 16), -(-cs["cols"] // 16))
     assert rec.work_group_size == 256
-    assert rec.native["kernel"].startswith("im2col_b")
+    assert rec.native["kernel"].startswith(("im2col_b", "im2col_vec_b"))
 
 
 @pytest.mark.parametrize("prec", ["S", "H"])
@@ -56,6 +56,59 @@ def test_im2col_large_vs_oracle_bitwise(ctx, prec):
     tb.im2col(ctx, c, h, w, kh, kw, 1, 1, 1, 1, 1, 1, im, col)
     want = orc.port_im2col(image, 0, c, h, w, kh, kw, 1, 1, 1, 1, 1, 1, np.zeros(rows * cols, dt), 0)
     assert np.array_equal(tb.buffer_read(col, 0, rows * cols).view(np.uint8), want.view(np.uint8))
+
+
+# Geometries for the register-transposed kernel (csrc/im2col.cuh
+# im2col_vec_kernel; rows a multiple of the 16-byte vector):
+# pixel tiles narrower and wider than a row, strides, dilations, negative
+# padding, a ragged last channel block, wide rows (fewer channels per CTA).
+STAGED = [
+    # c, h, w, kh, kw, ph, pw, sh, sw, dh, dw
+    (64, 56, 56, 3, 3, 1, 1, 1, 1, 1, 1),
+    (24, 30, 40, 3, 3, 1, 1, 2, 2, 1, 1),
+    (16, 9, 8, 3, 3, 2, 2, 1, 1, 2, 2),
+    (40, 23, 24, 1, 1, 0, 0, 1, 1, 1, 1),
+    (8, 13, 16, 5, 5, -1, 2, 2, 1, 1, 2),
+    (20, 12, 232, 3, 3, 1, 1, 1, 1, 1, 1),
+    (72, 5, 152, 2, 4, 0, 1, 1, 3, 2, 1),
+    (16, 7, 7, 3, 3, 1, 1, 1, 1, 1, 1),
+    (5, 9, 10, 3, 3, 1, 1, 1, 1, 1, 1),     # 45 rows: the tile kernel
+]
+
+
+def _vec_eligible(prec, geo):
+    """Mirror of tb_im2col's condition for the patch-staged H kernel."""
+    c, h, w, kh, kw, ph, pw, sh, sw, dh, dw = geo
+    if prec != "H":
+        return False
+    oh = (h + 2 * ph - (dh * (kh - 1) + 1)) // sh + 1
+    ow = (w + 2 * pw - (dw * (kw - 1) + 1)) // sw + 1
+    rows, tr = c * kh * kw, 64
+    pr = (255 // ow + 1) * sh + (kh - 1) * dh + 1
+    pwid = (ow - 1) * sw + (kw - 1) * dw + 1
+    nch = (tr - 1) // (kh * kw) + 2
+    return rows % 8 == 0 and nch * pr * pwid * 2 <= 15360
+
+
+@pytest.mark.parametrize("prec", ["S", "H"])
+@pytest.mark.parametrize("geo", STAGED)
+def test_im2col_vec_vs_oracle_bitwise(ctx, prec, geo):
+    c, h, w, kh, kw, ph, pw, sh, sw, dh, dw = geo
+    oh = (h + 2 * ph - (dh * (kh - 1) + 1)) // sh + 1
+    ow = (w + 2 * pw - (dw * (kw - 1) + 1)) // sw + 1
+    rows, cols = c * kh * kw, oh * ow
+    vec = 16 // orc.DTYPE[prec]().itemsize
+    rng = np.random.default_rng(c * 1000 + w)
+    dt = orc.DTYPE[prec]
+    image = rng.uniform(-1, 1, c * h * w).astype(dt)
+    im = _buf(ctx, P[prec], image)
+    sentinel = np.full(rows * cols + 64, 7, dt)
+    col = _buf(ctx, P[prec], sentinel)
+    tb.im2col(ctx, c, h, w, kh, kw, ph, pw, sh, sw, dh, dw, im, col)
+    assert ctx.last_launch.native["kernel"].startswith("im2col_vec_b" if _vec_eligible(prec, geo) else "im2col_b")
+    want = orc.port_im2col(image, 0, c, h, w, kh, kw, ph, pw, sh, sw, dh, dw, sentinel.copy(), 0)
+    got = tb.buffer_read(col, 0, col.length)
+    assert np.array_equal(got.view(np.uint8), want.view(np.uint8))
 
 
 def _conv2d(image, weights, pad, stride, dil):
