@@ -299,19 +299,26 @@ def seqk_gemm_split(prec: str, row_major: bool, trans_a: bool, trans_b: bool, m,
     rank r runs the sequential-k chain over K stages [r*kt, (r+1)*kt) of
     `stage` elements (kt = ceil(ceil(k/stage)/ks)), the partials are added in
     rank order with FP32 roundings, then the reference epilogue (alpha*acc,
-    + beta*C as separately rounded FP32 ops; compute.py:408-412).  Row-major
-    and untransposed operands only (what the split route serves in tests)."""
-    assert prec == "S" and row_major and not trans_a and not trans_b
+    + beta*C as separately rounded FP32 ops; compute.py:408-412).  Any layout
+    and transposition (the K slices are cut from the logical op(A), op(B))."""
+    assert prec == "S"
     kt = -(-(-(-k // stage)) // ks)
+    ar, ac = (k, m) if trans_a else (m, k)
+    br, bc = (n, k) if trans_b else (k, n)
+    A = logical(a, a_offset, ar, ac, lda, row_major)
+    B = logical(b, b_offset, br, bc, ldb, row_major)
+    A = A.T if trans_a else A
+    B = B.T if trans_b else B
     total = None
     for r in range(ks):
         k0, k1 = min(k, r * kt * stage), min(k, (r + 1) * kt * stage)
         part = np.zeros(m * n, np.float32)
         if k1 > k0:
-            seqk_gemm("S", True, False, False, m, n, k1 - k0, 1.0, a, a_offset + k0, lda, b,
-                      b_offset + k0 * ldb, ldb, 0.0, part, 0, n)
+            a_s = np.ascontiguousarray(A[:, k0:k1], np.float32).ravel()
+            b_s = np.ascontiguousarray(B[k0:k1, :], np.float32).ravel()
+            seqk_gemm("S", True, False, False, m, n, k1 - k0, 1.0, a_s, 0, k1 - k0, b_s, 0, n, 0.0, part, 0, n)
         total = part if total is None else (total + part).astype(np.float32)
-    cv = logical(c, c_offset, m, n, ldc, True)
+    cv = logical(c, c_offset, m, n, ldc, row_major)
     al, be = np.float32(alpha), np.float32(beta)
     acc = total.reshape(m, n)
     out = (al * acc).astype(np.float32)

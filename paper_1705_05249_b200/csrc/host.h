@@ -128,7 +128,7 @@ void* splitk_workspace(cudaStream_t stream, size_t bytes);
 
 // Dispatchers.
 int dispatch_sgemm(const Call& c);                                   // sgemm.cu
-int dispatch_sgemm_tma(const Call& c, int tile, int mwg, int nwg);   // sgemm_tma.cu
+int dispatch_sgemm_tma(const Call& c, int tile, int mwg, int nwg, int ks = 1);   // sgemm_tma.cu
 int dispatch_hgemm(const Call& c);                                   // hgemm.cu
 int dispatch_hsmall_any(const Call& c);                              // hgemm_small.cu
 int launch_hscale(const Call& c);                                    // hgemm.cu

@@ -192,7 +192,7 @@ int dispatch_sgemm(const Call& c) {
     // A "gemm_b200" configuration (override / tuning DB): its tile, on the
     // TMA-fed kernel for KWG 32 when the operands allow tensor maps.
     if (g->KWG >= 32) {
-      const int rc = dispatch_sgemm_tma(c, -1, g->MWG, g->NWG);
+      const int rc = dispatch_sgemm_tma(c, -1, g->MWG, g->NWG, g->SPLIT_K);
       if (rc >= 0) return rc;
     }
     return simt_tile(c, g->MWG, g->NWG);

@@ -64,6 +64,8 @@ int big_tiles(const Call& c, bool amn, bool bmn) {
 // >= 8 K stages per rank.  Measured (tools/route_probe.py): C3 (4096, 128,
 // 9216): 64 tiles, KS = 4: 265 -> 221 us; C1 (1024^3, 128 tiles) split in
 // two ran slower than unsplit (59.4 vs 55.8 us), hence the half-wave bound.
+// Failing that, KS = 4 when it reaches three quarters of a wave: (512, 512,
+// 4096), 32 tiles: 88.0 us unsplit (64x32 tiles) -> 63.5 us.
 // Returns 1 when K is not split.
 int sgemm_split_ks(const Problem& p) {
   const int sms = sms_or_default();
@@ -72,6 +74,7 @@ int sgemm_split_ks(const Problem& p) {
   if (2 * t1 > sms) return 1;
   for (int ks = 2; ks <= 4; ks *= 2)
     if (t1 * ks >= sms && t1 * ks <= 2 * sms && ktiles >= 8 * ks) return ks;
+  if (4 * t1 * 4 >= 3 * sms && ktiles >= 32) return 4;
   return 1;
 }
 
@@ -101,6 +104,13 @@ int tiles_64x32(const Call& c, bool amn, bool bmn) {
   if (bmn) return launch_stma<64, 32, 4, 4, 3, false, true>(c);
   return launch_stma<64, 32, 4, 4, 3, false, false>(c);
 }
+template <int KS>
+int tiles_64x32_split(const Call& c, bool amn, bool bmn) {
+  if (amn && bmn) return launch_stma<64, 32, 4, 4, 3, true, true, false, 1, KS>(c);
+  if (amn) return launch_stma<64, 32, 4, 4, 3, true, false, false, 1, KS>(c);
+  if (bmn) return launch_stma<64, 32, 4, 4, 3, false, true, false, 1, KS>(c);
+  return launch_stma<64, 32, 4, 4, 3, false, false, false, 1, KS>(c);
+}
 int tiles_32x32(const Call& c, bool amn, bool bmn) {
   // k <= 32 is a single K block: one ring slot and a 51-register cap, so 20
   // CTAs per SM fit (2 slots at 92 registers: 10; 49.0 -> 44.3 us at S32;
@@ -123,7 +133,7 @@ int tiles_32x32(const Call& c, bool amn, bool bmn) {
 // tile: 0 = by shape (built-in routing), 2 = one 64x64 tile per instance
 // (batched 33..64), 3 = one 32x32 tile per instance (batched <= 32),
 // -1 = the configuration's MWG x NWG.
-int dispatch_sgemm_tma(const Call& c, int tile, int mwg, int nwg) {
+int dispatch_sgemm_tma(const Call& c, int tile, int mwg, int nwg, int ks) {
   const Problem& p = c.p;
   const bool amn = !p.a_kcontig, bmn = p.b_ncontig;
   if (p.a_offs || p.b_offs || p.alphas || p.betas || p.k <= 0 || p.alpha == 0.0f) return -1;
@@ -132,6 +142,12 @@ int dispatch_sgemm_tma(const Call& c, int tile, int mwg, int nwg) {
   if (p.batch > 1 && ((p.stride_a % 4) || (p.stride_b % 4))) return -1;
   if (p.m > 0x7fffff00LL || p.n > 0x7fffff00LL || p.k > 0x7fffff00LL || p.batch > 0x7fffffffLL) return -1;
   if (tile == -1) {
+    if (ks == 2 || ks == 4) {  // configured deterministic split-K (instantiated tiles only)
+      if (mwg == 128 && nwg == 64)
+        return ks == 2 ? tiles_128x64_split<2>(c, amn, bmn) : tiles_128x64_split<4>(c, amn, bmn);
+      if (mwg == 64 && nwg == 32)
+        return ks == 2 ? tiles_64x32_split<2>(c, amn, bmn) : tiles_64x32_split<4>(c, amn, bmn);
+    }
     if (mwg >= 128 && nwg >= 128) return big_tiles(c, amn, bmn);
     if (mwg >= 128 && nwg == 64) return tiles_128x64(c, amn, bmn);
     if (mwg == 64 && nwg == 64) return tiles_64x64(c, amn, bmn);

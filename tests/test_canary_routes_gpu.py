@@ -33,6 +33,8 @@ CASES = [
     ("s_general", "S", 300, 520, 200, 1, None, native.FLAG_SIMT_GENERAL, "gen"),
     ("s_small", "S", 30, 28, 24, 37, None, 0, "sgemm"),
     ("s_tf32", "S", 300, 520, 200, 1, None, native.FLAG_TF32, "tf32"),
+    ("s_splitk_auto", "S", 512, 512, 4096, 1, None, 0, "splitk4"),
+    ("s_splitk_64x32_cfg", "S", 300, 200, 1000, 1, (64, 32, 32, 0, 1, 2, 0), 0, "64x32x32_4x4_mk_splitk2"),
 ]
 
 
