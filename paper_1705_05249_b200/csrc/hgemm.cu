@@ -74,25 +74,26 @@ int launch_hg_tma_stages(const Call& c, const CUtensorMap& ta, const CUtensorMap
   return launch_hg_layout<BN, true, true>(c, ta, tbm);
 }
 
-template <bool AMN, bool BMN>
+template <bool AMN, bool BMN, int BNP = 256>
 int launch_h2(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm, bool sync_waves) {
+  using Cfg = H2Cfg<BNP>;
   const Problem& p = c.p;
   const int tiles_m = static_cast<int>((p.m + 255) / 256);
-  const int tiles_n = static_cast<int>((p.n + H2_BN - 1) / H2_BN);
+  const int tiles_n = static_cast<int>((p.n + BNP - 1) / BNP);
   const int64_t total = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
-  auto kern = hgemm_tc_2sm_kernel<AMN, BMN>;
+  auto kern = hgemm_tc_2sm_kernel<AMN, BMN, BNP>;
   static SmemAttr attr;  // per instantiation, per device
-  if (int rc = ensure_smem(attr, kern, H2Cfg::SMEM_BYTES)) return rc;
+  if (int rc = ensure_smem(attr, kern, Cfg::SMEM_BYTES)) return rc;
   // Persistent clusters: as many pairs as can be co-resident (the wave
   // barrier assumes co-residency; the occupancy query sees only this
   // kernel's limits, hence the barrier's abandon flag).
-  static int max_pairs[64] = {0};
+  static int max_pairs[64] = {0};  // per instantiation, per device
   const int dev = current_device();
   if (max_pairs[dev] == 0) {
     cudaLaunchConfig_t q = {};
     q.gridDim = dim3(2);
-    q.blockDim = dim3(H2Cfg::THREADS);
-    q.dynamicSmemBytes = H2Cfg::SMEM_BYTES;
+    q.blockDim = dim3(Cfg::THREADS);
+    q.dynamicSmemBytes = Cfg::SMEM_BYTES;
     int v = 0;
     if (cudaOccupancyMaxActiveClusters(&v, kern, &q) != cudaSuccess || v < 1) {
       cudaGetLastError();
@@ -101,7 +102,7 @@ int launch_h2(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm, bool
     max_pairs[dev] = v;
   }
   const int64_t clusters = total < max_pairs[dev] ? total : max_pairs[dev];
-  dim3 grid(static_cast<unsigned>(2 * clusters)), block(H2Cfg::THREADS);
+  dim3 grid(static_cast<unsigned>(2 * clusters)), block(Cfg::THREADS);
   unsigned int* ctr = nullptr;
   if (sync_waves) {
     ctr = wave_counter(c.stream);  // nullptr: run without the (advisory) barrier
@@ -109,17 +110,18 @@ int launch_h2(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm, bool
       return check_launch("wave counter");
   }
   // group_m 8: measured best for pair tiles (also with the wave barrier)
-  if (int rc = launch_ex("hgemm_tc_2sm launch", kern, grid, block, H2Cfg::SMEM_BYTES, c.stream, 1, ta, tbm, p,
+  if (int rc = launch_ex("hgemm_tc_2sm launch", kern, grid, block, Cfg::SMEM_BYTES, c.stream, 1, ta, tbm, p,
                          tiles_m, tiles_n, cfg_group_m(c, 8), total, ctr))
     return rc;
   char name[64];
-  snprintf(name, sizeof(name), "hgemm_tc2sm_tma_256x256_%c%c%s", AMN ? 'm' : 'k', BMN ? 'n' : 'k',
+  snprintf(name, sizeof(name), "hgemm_tc2sm_tma_256x%d_%c%c%s", BNP, AMN ? 'm' : 'k', BMN ? 'n' : 'k',
            ctr ? "_ws" : "");
-  record(name, grid, block, 2, H2Cfg::SMEM_BYTES, total);
+  record(name, grid, block, 2, Cfg::SMEM_BYTES, total);
   return check_launch("hgemm_tc_2sm launch");
 }
 
-// pair: -1 = by shape, 0 = single-CTA kernel, 1 = CTA pair.
+// pair: -1 = by shape, 0 = single-CTA kernel, 1 = CTA pair (256 x 256),
+// 2 = CTA pair with the 256 x 512 tile.
 template <int BN>
 int dispatch_hgemm_bn(const Call& c, int pair) {
   const Problem& p = c.p;
@@ -143,13 +145,20 @@ int dispatch_hgemm_bn(const Call& c, int pair) {
     // vs 1150 / 1325 for the single-CTA kernel (tools/hbig_probe.py).  Below
     // that the barrier measured neutral and is left off.
     const bool huge = flop > 6e12;
-    const bool two_sm = pair < 0 ? (BN == 256 && !(c.flags & TB_FLAG_NO_2SM) && pair_tiles >= sms / 2) : pair == 1;
+    const bool two_sm = pair < 0 ? (BN == 256 && !(c.flags & TB_FLAG_NO_2SM) && pair_tiles >= sms / 2) : pair >= 1;
+    const bool wide = two_sm && pair == 2;
     const bool sync_waves = two_sm && (huge || (c.flags & TB_FLAG_WAVE_SYNC));
     const uint32_t bbox = two_sm ? 128 : BN;
     if (!bmn) rc = make_map(&tbm, B, p.k, p.n, p.batch, p.ldb, p.stride_b, 64, bbox);
     else rc = make_map(&tbm, B, p.n, p.k, p.batch, p.ldb, p.stride_b, 64, 64);
     if (rc != TB_OK) return rc;
     if (two_sm) {
+      if (wide) {
+        if (!amn && !bmn) return launch_h2<false, false, 512>(c, ta, tbm, sync_waves);
+        if (!amn && bmn) return launch_h2<false, true, 512>(c, ta, tbm, sync_waves);
+        if (amn && !bmn) return launch_h2<true, false, 512>(c, ta, tbm, sync_waves);
+        return launch_h2<true, true, 512>(c, ta, tbm, sync_waves);
+      }
       if (!amn && !bmn) return launch_h2<false, false>(c, ta, tbm, sync_waves);
       if (!amn && bmn) return launch_h2<false, true>(c, ta, tbm, sync_waves);
       if (amn && !bmn) return launch_h2<true, false>(c, ta, tbm, sync_waves);
@@ -325,7 +334,7 @@ int dispatch_hgemm(const Call& c) {
       const int rc = dispatch_hsplit(c, g->SPLIT_K > 8 ? 8 : g->SPLIT_K);
       if (rc >= 0) return rc;
     }
-    if (g->CTA_GROUP == 2 && tma_ok(c)) return dispatch_hgemm_bn<256>(c, 1);
+    if (g->CTA_GROUP == 2 && tma_ok(c)) return dispatch_hgemm_bn<256>(c, g->NWG >= 512 ? 2 : 1);
     if (g->NWG >= 256) return dispatch_hgemm_bn<256>(c, 0);
     if (g->NWG >= 128) return dispatch_hgemm_bn<128>(c, 0);
     return dispatch_hgemm_bn<64>(c, 0);

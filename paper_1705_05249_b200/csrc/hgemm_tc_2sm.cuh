@@ -28,18 +28,27 @@
 namespace tb {
 
 constexpr int H2_BN = 256;          // pair tile N (per-CTA B half = 128)
-constexpr int H2_STAGES = 6;
 
+// BNP: pair tile N.  256: one UMMA (N = 256) per K16 step, double-buffered
+// accumulators (2 x 256 TMEM columns), 6-stage ring.  512: two UMMAs per K16
+// step into TMEM columns [0, 256) and [256, 512) (each CTA holds B columns
+// n0 + 128 r + {0, 256}, 128 each), one accumulator (the whole TMEM, so the
+// epilogue is not overlapped with the next tile's MMAs), 4-stage ring of
+// 48 KB: 1/4 less operand traffic per FLOP (L2 -> SM and shared-memory fill).
+template <int BNP = 256>
 struct H2Cfg {
+  static constexpr int STAGES = BNP == 512 ? 4 : 6;
+  static constexpr int ACC = BNP == 512 ? 1 : 2;              // accumulator buffers
   static constexpr int A_BYTES = 128 * HG_BK * 2;            // 16 KB: own 128 A rows
-  static constexpr int B_BYTES = (H2_BN / 2) * HG_BK * 2;    // 16 KB: own 128 B columns
+  static constexpr int B_BYTES = (BNP / 2) * HG_BK * 2;      // 16 / 32 KB: own B columns
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_WARPS = 8, PROD_WARP = 8, MMA_WARP = 9;
   static constexpr int THREADS = 10 * 32;
-  static constexpr int TMEM_COLS = 512;                       // 2 x 256 accumulators
+  static constexpr int TMEM_COLS = 512;
   static constexpr int BAR_BYTES = 1024;
   static constexpr int EPI_BYTES = EPI_WARPS * EPI_WARP_FLOATS * 4;
-  static constexpr int SMEM_BYTES = 1024 + H2_STAGES * STAGE_BYTES + BAR_BYTES + EPI_BYTES;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + BAR_BYTES + EPI_BYTES;
+  static_assert(SMEM_BYTES <= 232448, "fits the 227 KB opt-in shared memory");
 };
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -127,12 +136,13 @@ __device__ __forceinline__ void wave_arrive(unsigned int* ctr) {
   asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
 }
 
-template <bool A_MN, bool B_MN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
+template <bool A_MN, bool B_MN, int BNP = 256>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg<BNP>::THREADS, 1)
     hgemm_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Problem p,
                         int tiles_m, int tiles_n, int group_m, int64_t total_tiles, unsigned int* wave_ctr) {
-  using C = H2Cfg;
-  constexpr int STAGES = H2_STAGES;
+  using C = H2Cfg<BNP>;
+  constexpr int STAGES = C::STAGES;
+  constexpr int ACC = C::ACC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_align1024(smem_raw);
   uint8_t* sA = smem;
@@ -156,7 +166,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < ACC; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * 32 * C::EPI_WARPS);
     }
@@ -196,7 +206,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
       int64_t z; int mt, nt;
       tile_coords(t, tiles_m, tiles_n, group_m, z, mt, nt);
       const int m0 = mt * 256 + static_cast<int>(rank) * 128;
-      const int n0 = nt * H2_BN + static_cast<int>(rank) * (H2_BN / 2);
+      const int n0 = nt * BNP + static_cast<int>(rank) * 128;
       const int zz = static_cast<int>(z);
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty[s], ph ^ 1);
@@ -211,11 +221,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
             tma_load_3d_2sm(a_dst, &tmA, &full[s], m0, k0, zz);
             tma_load_3d_2sm(a_dst + 8192, &tmA, &full[s], m0 + 64, k0, zz);
           }
-          if (!B_MN) {
-            tma_load_3d_2sm(b_dst, &tmB, &full[s], k0, n0, zz);
-          } else {
-            tma_load_3d_2sm(b_dst, &tmB, &full[s], n0, k0, zz);
-            tma_load_3d_2sm(b_dst + 8192, &tmB, &full[s], n0 + 64, k0, zz);
+#pragma unroll
+          for (int h = 0; h < BNP / 256; ++h) {  // 128 columns at n0 + 256 h -> b_dst + 16 KB h
+            if (!B_MN) {
+              tma_load_3d_2sm(b_dst + h * 16384, &tmB, &full[s], k0, n0 + 256 * h, zz);
+            } else {
+              tma_load_3d_2sm(b_dst + h * 16384, &tmB, &full[s], n0 + 256 * h, k0, zz);
+              tma_load_3d_2sm(b_dst + h * 16384 + 8192, &tmB, &full[s], n0 + 256 * h + 64, k0, zz);
+            }
           }
         }
         __syncwarp();
@@ -230,7 +243,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
     // =============== MMA issuer (leader CTA only) ===============
     // The whole warp runs the loop (uniform operands); one elected lane issues.
     if (leader) {
-      constexpr uint32_t idesc = umma_idesc_f16(256, H2_BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      constexpr uint32_t idesc = umma_idesc_f16(256, 256, A_MN ? 1 : 0, B_MN ? 1 : 0);
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
@@ -238,7 +251,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
       for (int64_t t = cluster_id; t < total_tiles; t += n_clusters) {
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * H2_BN);
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * 256);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
@@ -246,7 +259,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
           const uint32_t b_addr = smem_u32(sB + s * C::B_BYTES);
           const int ksteps = hg_ksteps(p.k, kb);
           if (elect_one()) {
-            hg_issue_kblock<A_MN, B_MN>(Mma2Sm{}, d_tmem, a_addr, b_addr, idesc, ksteps, kb == 0);
+#pragma unroll
+            for (int h = 0; h < BNP / 256; ++h)
+              hg_issue_kblock<A_MN, B_MN>(Mma2Sm{}, d_tmem + 256 * h, a_addr, b_addr + 16384 * h, idesc, ksteps,
+                                          kb == 0);
             tc2_commit_mc(&empty[s], 0x3);
           }
           __syncwarp();
@@ -254,7 +270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
         }
         if (elect_one()) tc2_commit_mc(&tfull[acc], 0x3);
         __syncwarp();
-        if (++acc == 2) { acc = 0; aph ^= 1; }
+        if (++acc == ACC) { acc = 0; aph ^= 1; }
       }
     }
   } else if (warp < C::EPI_WARPS) {
@@ -267,7 +283,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
     for (int64_t t = cluster_id; t < total_tiles; t += n_clusters) {
       int64_t z; int mt, nt;
       tile_coords(t, tiles_m, tiles_n, group_m, z, mt, nt);
-      const int64_t m0 = static_cast<int64_t>(mt) * 256 + rank * 128, n0 = static_cast<int64_t>(nt) * H2_BN;
+      const int64_t m0 = static_cast<int64_t>(mt) * 256 + rank * 128, n0 = static_cast<int64_t>(nt) * BNP;
       Epi epi;
       epi.alpha = inst_alpha(p, z);
       epi.beta = inst_beta(p, z);
@@ -275,12 +291,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
       const int64_t row0 = m0 + quad * 32;
       const int rows_valid = static_cast<int>(min64(32, p.m - row0));
       __half* Cz = static_cast<__half*>(p.c) + inst_off(p.c_off, p.stride_c, p.c_offs, z);
-      const int n_left = static_cast<int>(min64(H2_BN, p.n - n0));
+      const int n_left = static_cast<int>(min64(BNP, p.n - n0));
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(acc * H2_BN);
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(acc * 256);
 #pragma unroll 1
-      for (int cb = half * (H2_BN / 64); cb < (half + 1) * (H2_BN / 64); ++cb) {
+      for (int cb = half * (BNP / 64); cb < (half + 1) * (BNP / 64); ++cb) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(t_row + cb * 32, v);
         tmem_ld_wait();
@@ -289,7 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg::THREADS, 1)
       }
       tc_fence_before();
       mbar_arrive_cluster(&tempty[acc], 0);
-      if (++acc == 2) { acc = 0; aph ^= 1; }
+      if (++acc == ACC) { acc = 0; aph ^= 1; }
     }
   }
 
