@@ -52,8 +52,14 @@ _ROUTINES = {
 }
 
 #: Sub-blocks aim at this many bytes of the cut operand (and at most 8).
-CHUNK_BYTES = 32 << 20
-MAX_CHUNKS = 8
+# Sub-block size of the pipelined calls.  8192^3 HGEMM on pinned arrays
+# (tools/pcie_probe.py): 32 MB x 4 sub-blocks 6.2 ms, 16 MB x 8 6.05 ms,
+# 8 MB x 16 6.3 ms per call — the last sub-block's GEMM + D2H is the tail
+# after the final H2D, while below ~16 MB the interleaved H2D / D2H copies
+# lose rate (gaps between copies on the H2D stream).  Cutting B into column
+# blocks so the D2H could start during B's upload would need 2-D copies.
+CHUNK_BYTES = 16 << 20
+MAX_CHUNKS = 16
 
 _session_lock = threading.Lock()
 _session_ctx: Context | None = None
@@ -206,8 +212,10 @@ def _span(layout, rows: int, cols: int, off: int, ld: int, u0: int = 0, count: i
 
 def _download(finishers: list, C, lo: int, hi: int, slot: int) -> None:
     """Queue the D2H of C[lo:hi] through staging slot ``slot``.  The landing
-    of the sub-block two back used the same slot, so it completes first."""
-    if len(finishers) >= 2:
+    of the sub-block two back used the same slot, so it completes first
+    (pageable C only: a pinned C is copied into directly and nothing is
+    reused, so the host does not wait)."""
+    if len(finishers) >= 2 and not C.pinned:
         finishers.pop(0)()
     fin = C.download(lo, hi, slot)
     if fin is not None:
