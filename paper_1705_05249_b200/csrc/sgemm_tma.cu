@@ -106,10 +106,10 @@ int tiles_64x32(const Call& c, bool amn, bool bmn) {
 }
 template <int KS>
 int tiles_64x32_split(const Call& c, bool amn, bool bmn) {
-  if (amn && bmn) return launch_stma<64, 32, 4, 4, 3, true, true, false, 1, KS>(c);
-  if (amn) return launch_stma<64, 32, 4, 4, 3, true, false, false, 1, KS>(c);
-  if (bmn) return launch_stma<64, 32, 4, 4, 3, false, true, false, 1, KS>(c);
-  return launch_stma<64, 32, 4, 4, 3, false, false, false, 1, KS>(c);
+  if (amn && bmn) return launch_stma<64, 32, 4, 4, 3, true, true, false, 2, KS>(c);
+  if (amn) return launch_stma<64, 32, 4, 4, 3, true, false, false, 2, KS>(c);
+  if (bmn) return launch_stma<64, 32, 4, 4, 3, false, true, false, 2, KS>(c);
+  return launch_stma<64, 32, 4, 4, 3, false, false, false, 2, KS>(c);
 }
 int tiles_32x32(const Call& c, bool amn, bool bmn) {
   // k <= 32 is a single K block: one ring slot and a 51-register cap, so 20

@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
   }
 
   if constexpr (KS > 1) {
+    static_assert(BM * BN * 4 <= STAGES * Cfg::STAGE_BYTES + Cfg::T_BYTES, "partials parked in the ring");
     // ---- split-K: ranks 1.. park their partials, rank 0 adds them in order ----
     // Every stage this CTA loaded has been consumed, so the ring is free.
     constexpr int NACC = (PN ? TM : TM / 2) * (PN ? TN / 2 : TN);  // float2 per thread
