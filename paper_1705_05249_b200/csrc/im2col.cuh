@@ -114,8 +114,8 @@ __device__ __forceinline__ int im2col_div(int a, float inv) {
 // ---- patch-staged im2col with 16-byte stores ---------------------------------
 // The tile kernel above stores 2- or 4-byte values after a shared-memory
 // transpose and tests the padding per element: ~1.4 TB/s at the ResNet layer
-// even with L2-warm inputs, issue bound.  Here a CTA owns 256 consecutive
-// output pixels (a warp per 32) x TR column-matrix rows (TR = one 128-byte
+// even with L2-warm inputs, issue bound.  Here a CTA owns IM2COL_VQ = 128
+// consecutive output pixels (a warp per 32) x TR column-matrix rows (TR = one 128-byte
 // line per pixel column: 64 rows for H, 32 for S) and
 //   1. copies the image patch those rows and pixels touch — the channels of
 //      rows [r0, r0 + TR), image rows [y_lo, y_lo + PR), columns
@@ -133,13 +133,16 @@ __device__ __forceinline__ int im2col_div(int a, float inv) {
 // About 4 instructions per output element (the register-only variants with
 // per-element tap stepping and padding tests took ~33 and were issue bound).
 // ResNet layer (256 x 56 x 56, 3x3), H: 12.3 us L2-flushed / 7.9 us warm
-// against the tile kernel's 14.3-15.2 / 10.3.  Used for H only: for S (TR =
+// against the tile kernel's 14.3-15.2 / 10.3 (8 warps / 256 pixels per CTA:
+// 12.45 us; ncu showed SMs idle 42 % of the time with 3-4 CTAs each).  Used for H only: for S (TR =
 // 32 rows, patch over-fetch 1.4x) it measured 16.4 / 10.3 against 15.2 /
 // 10.3.
 // Host conditions (tbgemm.cu tb_im2col): rows a multiple of VEC, a 16-byte
 // aligned column matrix, the patch within IM2COL_PATCH_BYTES; otherwise the
 // tile kernel runs.  Same values either way.
-constexpr int IM2COL_PATCH_BYTES = 15360;  // + 32 KB of warp tiles: within 48 KB static
+constexpr int IM2COL_PATCH_BYTES = 15360;
+constexpr int IM2COL_VW = 4;                  // warps (32-pixel columns) per CTA
+constexpr int IM2COL_VQ = 32 * IM2COL_VW;     // output pixels per CTA
 
 struct Im2colPatch {
   int pw;        // patch columns (the padded x range of an output row)
@@ -147,18 +150,20 @@ struct Im2colPatch {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(IM2COL_VQ)
     im2col_vec_kernel(const T* __restrict__ im, T* __restrict__ col, Im2colGeom g, Im2colPatch pp) {
   constexpr int VEC = 16 / static_cast<int>(sizeof(T));  // elements per 16-byte vector
   constexpr int TR = 8 * VEC;                              // rows per CTA: 128 bytes per pixel
   __shared__ __align__(16) T patch[IM2COL_PATCH_BYTES / sizeof(T)];
   __shared__ __align__(16) int roff[TR];
-  __shared__ __align__(128) uint4 tiles[8][32 * 8];  // per warp: 32 pixels x 8 vectors
+  __shared__ __align__(128) uint4 tiles[IM2COL_VW][32 * 8];  // per warp: 32 pixels x 8 vectors
+  constexpr int NT = IM2COL_VQ;
+  static_assert(NT >= TR, "one thread per row-offset entry");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rows = static_cast<int>(g.rows), cols = static_cast<int>(g.cols);
-  const int q0 = static_cast<int>(blockIdx.x) * 256, r0 = static_cast<int>(blockIdx.y) * TR;
+  const int q0 = static_cast<int>(blockIdx.x) * IM2COL_VQ, r0 = static_cast<int>(blockIdx.y) * TR;
   const int PW = pp.pw, kk = g.kh * g.kw;
-  const int oy_lo = q0 / g.out_w, oy_hi = min(q0 + 255, cols - 1) / g.out_w;
+  const int oy_lo = q0 / g.out_w, oy_hi = min(q0 + IM2COL_VQ - 1, cols - 1) / g.out_w;
   const int y_lo = oy_lo * g.stride_h - g.pad_h;
   const int PR = (oy_hi - oy_lo) * g.stride_h + (g.kh - 1) * g.dil_h + 1;
   const int c_lo = r0 / kk, c_hi = (min(r0 + TR, rows) - 1) / kk;
@@ -166,11 +171,11 @@ __global__ void __launch_bounds__(256)
   const int plane = g.height * g.width;
   const int total = (c_hi - c_lo + 1) * PR * PW;
   const float inv_pw = __frcp_rn(static_cast<float>(PW)), inv_pr = __frcp_rn(static_cast<float>(PR));
-  for (int e0 = tid; e0 < total; e0 += 4 * 256) {
+  for (int e0 = tid; e0 < total; e0 += 4 * NT) {
     T v[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int e = e0 + u * 256;
+      const int e = e0 + u * NT;
       const int row = im2col_div(e, inv_pw), x = e - row * PW - g.pad_w;
       const int cl = im2col_div(row, inv_pr), y = y_lo + row - cl * PR;
       const bool ok = e < total && static_cast<unsigned>(y) < static_cast<unsigned>(g.height) &&
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(256)
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (e0 + u * 256 < total) patch[e0 + u * 256] = v[u];
+      if (e0 + u * NT < total) patch[e0 + u * NT] = v[u];
   }
   if (tid < TR) {
     const int r = min(r0 + tid, rows - 1);

@@ -84,7 +84,7 @@ def _vec_eligible(prec, geo):
     oh = (h + 2 * ph - (dh * (kh - 1) + 1)) // sh + 1
     ow = (w + 2 * pw - (dw * (kw - 1) + 1)) // sw + 1
     rows, tr = c * kh * kw, 64
-    pr = (255 // ow + 1) * sh + (kh - 1) * dh + 1
+    pr = (127 // ow + 1) * sh + (kh - 1) * dh + 1   # IM2COL_VQ = 128 pixels per CTA
     pwid = (ow - 1) * sw + (kw - 1) * dw + 1
     nch = (tr - 1) // (kh * kw) + 2
     return rows % 8 == 0 and nch * pr * pwid * 2 <= 15360
