@@ -558,4 +558,149 @@ __global__ void __launch_bounds__(Hs32Cfg::THREADS, 1)
   }
 }
 
+// ---- 64-wide instances through TMA -----------------------------------------
+// m, n, k <= 64 over a strided batch: P = 2 instances per 128 x 128 UMMA tile
+// (instance 0 in rows / columns 0-63, instance 1 in 64-127; the product's
+// diagonal blocks are the results), each operand ONE 3-D TMA box {64, 64, 2}
+// per tile — a 64-element row is exactly one 128-byte SWIZZLE_128B row, so
+// the tiles are the ordinary 128-row SW128 layouts (K-major: 8-row atoms,
+// MN-major: two 64-element chunks 8 KB apart) and hg_issue_kblock issues
+// them.  Replaces 128 producer threads of cp.async (5-7 stages) with one
+// elected thread and a 6-stage ring of 32 KB.  Same K16 sequence per element
+// as every other H kernel: bitwise equal.
+struct Hs64Cfg {
+  static constexpr int P = 2, MI = 64, NI = 64, BN = 128;
+  static constexpr int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 32 KB
+  static constexpr int STAGES = 6;
+  static constexpr int ACC = 4;
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int EPI_WARPS = 8, PROD_WARP = 8, MMA_WARP = 9;
+  static constexpr int THREADS = 10 * 32;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 1024 + EPI_WARPS * EPI_WARP_FLOATS * 4;
+  static_assert(SMEM_BYTES <= 232448, "fits the 227 KB opt-in shared memory");
+};
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(Hs64Cfg::THREADS, 1)
+    hgemm_tc_small64_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                                Problem p, int64_t total_tiles) {
+  using C = Hs64Cfg;
+  constexpr int STAGES = C::STAGES, P = C::P, BN = C::BN, ACC = C::ACC, MI = C::MI, NI = C::NI;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_align1024(smem_raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + ACC;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + ACC);
+  float* epi_stage = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES + 1024);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < ACC; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 32 * C::EPI_WARPS);  // all 8 epilogue warps per tile
+    }
+    fence_mbar_init();
+  }
+  if (warp == C::PROD_WARP && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == C::MMA_WARP) tmem_alloc(tmem_holder, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  grid_dep_wait();  // prologue above overlapped the previous kernel (PDL)
+  grid_dep_launch();
+  const int m = static_cast<int>(p.m), n = static_cast<int>(p.n);
+
+  if (warp == C::PROD_WARP) {
+    // ===================== producer: 2 TMA boxes per tile =====================
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      mbar_wait(&empty[s], ph ^ 1);
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+        const int z0 = static_cast<int>(t * P);
+        tma_load_3d(sA + s * C::A_BYTES, &tmA, &full[s], 0, 0, z0);
+        tma_load_3d(sB + s * C::B_BYTES, &tmB, &full[s], 0, 0, z0);
+      }
+      __syncwarp();
+      if (++s == STAGES) { s = 0; ph ^= 1; }
+    }
+  } else if (warp == C::MMA_WARP) {
+    // ===================== MMA issuer =====================
+    constexpr uint32_t idesc = umma_idesc_f16(128, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+    const int ksteps = hg_ksteps(p.k, 0);
+    int s = 0, acc = 0;
+    uint32_t ph = 0, aph = 0;
+    for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], aph ^ 1);
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+      const uint32_t a_addr = smem_u32(sA + s * C::A_BYTES);
+      const uint32_t b_addr = smem_u32(sB + s * C::B_BYTES);
+      if (elect_one()) {
+        hg_issue_kblock<A_MN, B_MN>(Mma1Sm{}, d_tmem, a_addr, b_addr, idesc, ksteps, true);
+        tc_commit(&empty[s]);
+        tc_commit(&tfull[acc]);
+      }
+      __syncwarp();
+      if (++s == STAGES) { s = 0; ph ^= 1; }
+      if (++acc == ACC) { acc = 0; aph ^= 1; }
+    }
+  } else if (warp < C::EPI_WARPS) {
+    // ===== epilogue: warp w -> TMEM lanes of quadrant w%4 (instance (w%4)/2), columns half w/4 =====
+    const int quad = warp & 3;
+    const int half = warp >> 2;
+    const int slot = (quad * 32) / MI;
+    int acc = 0;
+    uint32_t aph = 0;
+    float* stage = epi_stage + warp * EPI_WARP_FLOATS;
+    for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      const int64_t zi = t * P + slot;
+      const bool inst_ok = zi < p.batch;
+      Epi epi;
+      epi.alpha = inst_ok ? inst_alpha(p, zi) : 0.0f;
+      epi.beta = inst_ok ? inst_beta(p, zi) : 0.0f;
+      epi.skip_ab = (epi.alpha == 0.0f);
+      __half* Cz = static_cast<__half*>(p.c) + (inst_ok ? inst_off(p.c_off, p.stride_c, p.c_offs, zi) : 0);
+      const int row0 = quad * 32 - slot * MI;
+      const int rows_valid = inst_ok ? min(32, m - row0) : 0;
+      const int cols_valid = n - half * 32;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                             static_cast<uint32_t>(acc * BN + slot * NI + half * 32);
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(t_row, v);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);  // accumulator drained (values in registers)
+      if (++acc == ACC) { acc = 0; aph ^= 1; }
+      if (rows_valid > 0 && cols_valid > 0)
+        epi_store_block<32>(stage, v, Cz + static_cast<int64_t>(half * 32) * p.ldc + row0, p.ldc, rows_valid,
+                            cols_valid, epi, lane);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == C::MMA_WARP) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
 }  // namespace tb

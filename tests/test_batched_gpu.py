@@ -173,7 +173,8 @@ def test_full_size_batch_16384(ctx, prec, size):
 @pytest.mark.parametrize("layout", [Layout.COL_MAJOR, Layout.ROW_MAJOR])
 @pytest.mark.parametrize("ta", [Transpose.NO, Transpose.YES])
 @pytest.mark.parametrize("tbt", [Transpose.NO, Transpose.YES])
-@pytest.mark.parametrize("shape", [(32, 32, 32), (64, 64, 64), (20, 50, 77), (64, 17, 300), (8, 64, 1)])
+@pytest.mark.parametrize("shape", [(32, 32, 32), (64, 64, 64), (20, 50, 77), (64, 17, 300), (8, 64, 1),
+                                   (48, 40, 64), (64, 32, 40)])
 def test_small_path_bitwise_equals_general_path(ctx, prec, layout, ta, tbt, shape):
     """The small-instance kernels (packed tcgen05 for H, TMA-fed FFMA2 tiles
     for S) give the same bits as the general kernels forced via flags."""
@@ -201,6 +202,8 @@ def test_small_path_bitwise_equals_general_path(ctx, prec, layout, ta, tbt, shap
         (prec is Precision.H and all(v % 8 == 0 for v in (ea, eb, lda, ldb)))
     if prec is Precision.H:
         assert "small" in kernels[0], kernels
+        if aligned and max(m, n, k) <= 64:   # one TMA box per operand per tile (32- or 64-wide kernel)
+            assert kernels[0].endswith("_tma"), kernels
     elif aligned and m <= 32 and n <= 32:
         # strided S batches of <= 32x32 instances: one TMA-fed 32x32 tile each
         assert kernels[0].startswith("sgemm_tma_32x32"), kernels
