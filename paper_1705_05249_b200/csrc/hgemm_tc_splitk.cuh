@@ -403,9 +403,15 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
       }
       if (et == 0 && t == cluster_id) SK_STAMP(9);
       // (2b) done reading every rank's partial of this tile: release the
-      // buffers before the (slow to drain) global stores
-      sk_fence_cluster();
-      for (uint32_t q = 0; q < ks; ++q) sk_arrive_remote_relaxed(sk_mapa(re_local, q));
+      // buffers before the (slow to drain) global stores.  Not after the
+      // last tile in workspace mode: nothing waits for it, no peer reads this
+      // CTA's shared memory, and the kernel then ends without a cluster
+      // barrier (the last remote operation aimed at this CTA, a red_full
+      // arrival, has landed once its red_full wait returned).
+      if (ws_base == nullptr || t + n_clusters < total_tiles) {
+        sk_fence_cluster();
+        for (uint32_t q = 0; q < ks; ++q) sk_arrive_remote_relaxed(sk_mapa(re_local, q));
+      }
       if (et == 0 && t == cluster_id) SK_STAMP(10);
       // (2c) epilogue and 16-byte stores
 #pragma unroll
@@ -458,7 +464,8 @@ __global__ void __launch_bounds__(SkCfg<TMA>::THREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
-  sk_cluster_sync();  // no CTA leaves while a peer may still read its partials
+  // DSMEM mode: no CTA leaves while a peer may still read its partials
+  if (ws == nullptr) sk_cluster_sync();
   if (threadIdx.x == 0) SK_STAMP(8);
 }
 
