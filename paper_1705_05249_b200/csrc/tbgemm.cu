@@ -406,18 +406,18 @@ int tb_im2col(int prec, int64_t channels, int64_t height, int64_t width, int64_t
   if (prec == TB_PREC_H) {
     const int es = prec == TB_PREC_S ? 4 : 2, vec = 16 / es, tr = 8 * vec;  // rows per CTA
     const int kk = g.kh * g.kw;
-    // worst-case patch of 256 consecutive pixels x tr rows
-    const int64_t oy_span = 255 / g.out_w + 2;
+    // worst-case patch of IM2COL_VQ consecutive pixels x tr rows
+    const int64_t oy_span = (IM2COL_VQ - 1) / g.out_w + 2;
     const int64_t pr = (oy_span - 1) * g.stride_h + static_cast<int64_t>(g.kh - 1) * g.dil_h + 1;
     const int64_t pw = static_cast<int64_t>(g.out_w - 1) * g.stride_w + static_cast<int64_t>(g.kw - 1) * g.dil_w + 1;
     const int64_t nch = (tr - 1) / kk + 2;
-    const int64_t r_chunks = (g.rows + tr - 1) / tr, q_blocks = (g.cols + 255) / 256;
+    const int64_t r_chunks = (g.rows + tr - 1) / tr, q_blocks = (g.cols + IM2COL_VQ - 1) / IM2COL_VQ;
     if (g.rows % vec == 0 && aligned_elems(col, col_off, es, 16) && nch * pr * pw * es <= IM2COL_PATCH_BYTES &&
         pw <= 1024 && pr <= 1024 && r_chunks <= 65535 && q_blocks < 0x7fffffff) {
       Im2colPatch pp;
       pp.pw = static_cast<int>(pw);
       pp.r_chunks = static_cast<int>(r_chunks);
-      const dim3 grid2(static_cast<unsigned>(q_blocks), static_cast<unsigned>(r_chunks)), block2(256);
+      const dim3 grid2(static_cast<unsigned>(q_blocks), static_cast<unsigned>(r_chunks)), block2(IM2COL_VQ);
       im2col_vec_kernel<uint16_t><<<grid2, block2, 0, st>>>(static_cast<const uint16_t*>(im) + im_off,
                                                             static_cast<uint16_t*>(col) + col_off, g, pp);
       name = "im2col_vec_b16";
