@@ -108,10 +108,15 @@ __global__ void __launch_bounds__(TmaSgemmCfg<BM, BN, BK, TM, TN, STAGES, A_MN, 
   const int64_t per_inst = static_cast<int64_t>(tiles_m) * tiles_n;
   const int64_t tile_id = blockIdx.x / KS;
   const int krank = KS > 1 ? static_cast<int>(blockIdx.x % KS) : 0;
-  const int z = static_cast<int>(tile_id / per_inst);
-  int mt, nt;
-  {
-    const int r = static_cast<int>(tile_id - z * per_inst);
+  // one tile per instance (the batched small shapes): no 64-bit division
+  // and no raster arithmetic in the prologue of these short-lived CTAs
+  // (ncu: the division and its branches were among the top stall sites)
+  // (the host keeps blocks * KS < 2^31, so 32-bit arithmetic is exact)
+  const int z = per_inst == 1 ? static_cast<int>(tile_id)
+                              : static_cast<int>(tile_id) / static_cast<int>(per_inst);
+  int mt = 0, nt = 0;
+  if (per_inst != 1) {
+    const int r = static_cast<int>(tile_id) - z * static_cast<int>(per_inst);
     const int group_size = group_m * tiles_n;
     const int g = r / group_size;
     const int first_m = g * group_m;
