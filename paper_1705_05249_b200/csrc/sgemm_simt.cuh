@@ -146,7 +146,15 @@ __device__ __forceinline__ void simt_store_stage(float* __restrict__ s, const fl
 __device__ __forceinline__ void tile_coords(int64_t bid, int tiles_m, int tiles_n, int group_m,
                                             int64_t& z, int& mt, int& nt) {
   const int64_t per_inst = static_cast<int64_t>(tiles_m) * tiles_n;
-  z = bid / per_inst;
+  if (per_inst == 1) {  // one tile per instance: no division (short-lived CTAs)
+    z = bid;
+    mt = nt = 0;
+    return;
+  }
+  // 32-bit division when the tile index allows (the usual case)
+  z = (bid < 0x7fffffffLL && per_inst < 0x7fffffffLL)
+          ? static_cast<int64_t>(static_cast<int>(bid) / static_cast<int>(per_inst))
+          : bid / per_inst;
   const int r = static_cast<int>(bid - z * per_inst);
   const int group_size = group_m * tiles_n;
   const int g = r / group_size;
