@@ -58,24 +58,35 @@ int big_tiles(const Call& c, bool amn, bool bmn) {
 // Deterministic split-K for the 128x64 tile (clusters of KS CTAs, DSMEM
 // reduction in rank order; sgemm_tma.cuh).  KS is a pure function of the
 // per-instance shape (m, n, k) and the SM count — never of the batch — so
-// single, batched and looped calls agree bitwise: when one instance's
-// 128x64 tiles fill less than half the SMs, the smallest KS in {2, 4} that
-// brings them to at least one wave (and at most two CTAs per SM), keeping
-// >= 8 K stages per rank.  Measured (tools/route_probe.py): C3 (4096, 128,
-// 9216): 64 tiles, KS = 4: 265 -> 221 us; C1 (1024^3, 128 tiles) split in
-// two ran slower than unsplit (59.4 vs 55.8 us), hence the half-wave bound.
-// Failing that, KS = 4 when it reaches three quarters of a wave: (512, 512,
-// 4096), 32 tiles: 88.0 us unsplit (64x32 tiles) -> 63.5 us.
+// single, batched and looped calls agree bitwise.  Only shapes whose 128x64
+// tiles fill at most half the SMs split; among KS in {1, 2, 4} (each rank
+// keeping >= 16 K stages: shorter chains are fixed-cost bound — C3b (64,
+// 3136, 576), 18 stages, ran 26.5 us split in two against 18.4 us on the
+// unsplit 64x32 tiles) the one with the fewest waves of work per SM,
+// ceil(tiles * KS / SMs) / KS, wins, ties going to the smaller KS (one CTA
+// per SM beats two sharing it).  Measured (tools/route_probe.py, L2 flushed):
+// C3 (4096, 128, 9216), 64 tiles: KS 2 215 us / KS 4 223 us / unsplit 265;
+// (768, 768, 2048), 72 tiles: KS 2 59.5 / KS 4 90.2; (512, 512, 4096), 32
+// tiles: KS 4 63.5 / unsplit 88.0; (300, 520, 4096), 25 tiles: KS 4 63.5 /
+// KS 2 102.4 / unsplit 86.1; C1 (1024^3, 128 tiles) ties and stays unsplit
+// (split in two measured 59.4 against 55.8 us).
 // Returns 1 when K is not split.
 int sgemm_split_ks(const Problem& p) {
   const int sms = sms_or_default();
   const int64_t t1 = ((p.m + 127) / 128) * ((p.n + 63) / 64);
   const int64_t ktiles = (p.k + 31) / 32;
   if (2 * t1 > sms) return 1;
-  for (int ks = 2; ks <= 4; ks *= 2)
-    if (t1 * ks >= sms && t1 * ks <= 2 * sms && ktiles >= 8 * ks) return ks;
-  if (4 * t1 * 4 >= 3 * sms && ktiles >= 32) return 4;
-  return 1;
+  int best = 1;
+  int64_t best_waves = (t1 + sms - 1) / sms;  // cost = waves / ks, compared as fractions
+  for (int ks = 2; ks <= 4; ks *= 2) {
+    if (ktiles < 16 * ks) break;
+    const int64_t waves = (t1 * ks + sms - 1) / sms;
+    if (waves * best < best_waves * ks) {
+      best = ks;
+      best_waves = waves;
+    }
+  }
+  return best;
 }
 
 template <int KS>

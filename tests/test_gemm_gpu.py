@@ -8,6 +8,8 @@ Bars:
 * no writes outside the declared C range (test_level3.py:141-159).
 """
 
+import re
+
 import numpy as np
 import pytest
 
@@ -152,6 +154,22 @@ def test_direct_and_indirect_bitwise_equal(ctx, prec):
                             kernel=kernel)
                     outs.append(tb.buffer_read(c, 0, m * n))
                     kernels.append(ctx.last_launch.native["kernel"])
+                ks = re.search(r"_splitk(\d+)", kernels[1])
+                if ks is not None and prec == "S":
+                    # the TMA route splits K (S split-K: sgemm_tma.cu sgemm_split_ks);
+                    # each route then matches its own oracle bitwise
+                    order = "F"
+                    lda, ldb = av.shape[0], bv.shape[0]
+                    for out, split in ((outs[0], None), (outs[1], int(ks.group(1)))):
+                        want = np.zeros(m * n, np.float32)
+                        args = ("S", False, ta == "t", tbn == "t", m, n, k, 1.0, av.reshape(-1, order=order), 0,
+                                lda, bv.reshape(-1, order=order), 0, ldb, 0.0, want, 0, m)
+                        if split is None:
+                            orc.seqk_gemm(*args)
+                        else:
+                            orc.seqk_gemm_split(*args, split)
+                        assert out.tobytes() == want.tobytes(), kernels
+                    continue
                 assert outs[0].tobytes() == outs[1].tobytes(), kernels
                 if prec == "H" and m % 8 == 0 and k % 8 == 0 and n % 8 == 0:
                     assert "ldg" in kernels[0] and "tma" in kernels[1], kernels

@@ -35,7 +35,7 @@ def _draw(rng, i):
         m, n, k = int(rng.integers(1200, 2400)), int(rng.integers(1200, 2400)), int(rng.integers(64, 200))
     elif kind == 4:    # tall-skinny
         m, n, k = int(rng.integers(2000, 5000)), int(rng.integers(1, 40)), int(rng.integers(10, 300))
-    else:              # mid-size, longer K (S three-quarter-wave split)
+    else:              # mid-size, longer K (S split-K)
         m, n, k = int(rng.integers(300, 700)), int(rng.integers(300, 700)), int(rng.integers(1000, 2500))
     prec = "H" if rng.random() < 0.5 else "S"
     layout = Layout.ROW_MAJOR if rng.random() < 0.5 else Layout.COL_MAJOR

@@ -26,8 +26,8 @@ def _buf(ctx, arr):
 @pytest.mark.parametrize("layout", [Layout.ROW_MAJOR, Layout.COL_MAJOR])
 @pytest.mark.parametrize("ta,tbn", [("n", "n"), ("t", "n"), ("n", "t")])
 def test_mid_size_long_k_splits_bitwise(ctx, layout, ta, tbn):
-    """(512, 512, 4096): 32 tiles of 128 x 64, KS = 4 (three quarters of a
-    wave; 88 -> 63.5 us measured)."""
+    """(512, 512, 4096): 32 tiles of 128 x 64, KS = 4 (88 -> 63.5 us
+    measured)."""
     T = {"n": Transpose.NO, "t": Transpose.YES}
     m, n, k = 512, 512, 4096
     rng = np.random.default_rng(77)
@@ -72,13 +72,36 @@ def test_split_batched_equals_loop_bitwise(ctx):
     assert tb.buffer_read(cb, 0, cb.length).tobytes() == tb.buffer_read(cl, 0, cl.length).tobytes()
 
 
-def test_just_below_three_quarters_of_a_wave_is_not_split(ctx):
-    # 128x64 tiles: 3 x 9 = 27 per instance, 27 * 4 < 0.75 * 148
-    m, n, k = 300, 520, 4096
-    rng = np.random.default_rng(79)
-    a = _buf(ctx, rng.uniform(-1, 1, m * k).astype(np.float32))
-    b = _buf(ctx, rng.uniform(-1, 1, k * n).astype(np.float32))
+# (m, n, k) -> split factor of the built-in route (sgemm_tma.cu sgemm_split_ks
+# on 148 SMs: fewest waves of work per SM, ties to the smaller factor)
+ROUTE_KS = [
+    ((4096, 128, 9216), 2),   # C3: 64 tiles
+    ((768, 768, 2048), 2),    # 72 tiles
+    ((512, 512, 4096), 4),    # 32 tiles
+    ((300, 520, 4096), 4),    # 25 tiles
+    ((1024, 1024, 1024), 1),  # C1: 128 tiles, more than half the SMs
+    ((300, 520, 200), 1),     # too few K stages per rank
+    ((64, 3136, 576), 1),     # C3b: 18 K stages, the 64x32 tiles instead
+]
+
+
+@pytest.mark.parametrize("shape,ks", ROUTE_KS)
+def test_split_factor_rule_and_bits(ctx, shape, ks):
+    m, n, k = shape
+    rng = np.random.default_rng(m + n + k)
+    av = rng.uniform(-1, 1, m * k).astype(np.float32)
+    bv = rng.uniform(-1, 1, k * n).astype(np.float32)
+    a, b = _buf(ctx, av), _buf(ctx, bv)
     c = tb.buffer_alloc(ctx, S, m * n)
     tb.gemm(ctx, Layout.ROW_MAJOR, Transpose.NO, Transpose.NO, m, n, k, 1.0, a, b, 0.0, c)
-    if ctx.device.compute_units >= 148:
-        assert "splitk" not in ctx.last_launch.native["kernel"], ctx.last_launch.native
+    kern = ctx.last_launch.native["kernel"]
+    if ctx.device.compute_units == 148:
+        assert (f"splitk{ks}" in kern) if ks > 1 else ("splitk" not in kern), kern
+    want = np.zeros(m * n, np.float32)
+    mt = re.search(r"_splitk(\d+)", kern)
+    if mt:
+        orc.seqk_gemm_split("S", True, False, False, m, n, k, 1.0, av, 0, k, bv, 0, n, 0.0, want, 0, n,
+                            int(mt.group(1)))
+    else:
+        orc.seqk_gemm("S", True, False, False, m, n, k, 1.0, av, 0, k, bv, 0, n, 0.0, want, 0, n)
+    assert tb.buffer_read(c, 0, m * n).tobytes() == want.tobytes(), kern
