@@ -249,6 +249,15 @@ def tune(task: TuningTask, ctx: Context) -> TuningRun:
     if explored:
         harness.prewarm(explored[0])
     measurements = [measure(cfg, task, ctx, harness) for cfg in explored]
+    # The gemm_b200 built-in route is timed first, right after the pre-warm,
+    # while the clocks are still settling under the power cap (8192^3 HGEMM:
+    # 986 us first against ~720 us later in one run): time it again last and
+    # keep the faster of the two, so "tuned vs built-in" compares like with like.
+    if (task.kernel_family == "gemm_b200" and explored and is_b200_auto(explored[0])
+            and measurements[0].status == "ok"):
+        again = measure(explored[0], task, ctx, harness)
+        if again.status == "ok" and again.mean_time < measurements[0].mean_time:
+            measurements[0] = again
     ok = [m for m in measurements if m.status == "ok"]
     if not ok:
         raise TuningError(f"no valid configuration for device {task.device.name!r} "
