@@ -344,13 +344,21 @@ int dispatch_hgemm(const Call& c) {
     const int rc = dispatch_hsplit(c, ks);
     if (rc >= 0) return rc;
   }
-  // Fewer tiles than SMs: narrow the UMMA N extent (results are independent
-  // of it — tests/test_gemm_gpu.py) so more CTAs share the work.  A pure
-  // function of the shape (never of batch for the per-element sequence).
+  // Fewer 128 x 256 tiles than SMs: narrow the UMMA N extent when that
+  // reduces the tile-waves of work, waves(BN) * BN, ties to the wider tile
+  // (results are independent of it — tests/test_gemm_gpu.py).  2048^3: 128
+  // tiles of 128 x 256 in one wave, 24.5 us, against 256 tiles of 128 x 128
+  // in 1.7 waves, 28.7 us (the earlier "narrow while tiles < SMs" rule);
+  // 1536^2 x 4096: 128 x 128 28.7 us against 128 x 64 43.0 us; 1024^3 keeps
+  // 128 x 64 (one wave of 128 tiles).  With at least a wave of wide tiles
+  // the wide (or CTA-pair) kernel stays: its tiles are the efficient ones.
   const int sms = sms_or_default();
   auto tiles = [&](int b) { return ((p.m + HG_BM - 1) / HG_BM) * ((p.n + b - 1) / b) * p.batch; };
+  auto cost = [&](int b) { return ((tiles(b) + sms - 1) / sms) * b; };
   int bn = 256;
-  while (bn > 64 && tiles(bn) < sms) bn /= 2;
+  if (tiles(256) < sms)
+    for (int b = 128; b >= 64; b /= 2)
+      if (cost(b) < cost(bn)) bn = b;
   if (bn == 256) return dispatch_hgemm_bn<256>(c, -1);
   if (bn == 128) return dispatch_hgemm_bn<128>(c, -1);
   return dispatch_hgemm_bn<64>(c, -1);
