@@ -3,7 +3,8 @@
 //
 // For problems with fewer 128x128 output tiles than SMs and a long K (BASELINE
 // config C3 (4096, 128, 9216): 32 tiles, 144 K blocks) the single-CTA kernel
-// leaves most SMs idle.  Here a cluster of KS CTAs (KS = 2..8, a pure function
+// leaves most SMs idle.  Here a cluster of KS CTAs (KS = 2..8 — the built-in
+// route stops at 4, convgemm and configurations use 8 — a pure function
 // of (m, n, k) and the SM count — never of the batch, so single, batched and
 // looped calls of one shape stay bitwise consistent) shares each 128 x 128
 // tile: CTA r accumulates K blocks r, r+KS, r+2KS, ... in its own TMEM (same producer / MMA pipeline and

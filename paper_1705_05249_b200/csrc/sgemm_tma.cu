@@ -180,11 +180,15 @@ int dispatch_sgemm_tma(const Call& c, int tile, int mwg, int nwg, int ks) {
   // 66 TFLOP/s at 8192^3); below that 64x64 tiles of 4x8 (8x4) micro-tiles
   // keep every SM busy (1024^3 37.6, C3 (4096,128,9216) 34.8 TFLOP/s).
   const bool one_tile = p.m <= 64 && p.n <= 64;  // batched small instances: one 64x64 tile each
-  if (tile == 0 && tiles128 >= 4 * sms && !one_tile) return big_tiles(c, amn, bmn);
+  // (3.5 waves and more: 3072^3 1028 us big tiles against 1091 on 64x64)
+  if (tile == 0 && 2 * tiles128 >= 7 * sms && !one_tile) return big_tiles(c, amn, bmn);
   // fewer 64x64 tiles than SMs (e.g. C3 (64, 3136, 576): 49 tiles): 64x32
   // tiles of 4x4 (21 -> 14 us there; tools/sgemm_ms_bench.cu)
   const int64_t tiles64 = ((p.m + 63) / 64) * ((p.n + 63) / 64) * p.batch;
   if (tile == 0 && tiles64 < sms) return tiles_64x32(c, amn, bmn);
+  // at most 64 rows: 128-row tiles would be half empty (16384 x 64 x 2048
+  // row-major: 64x64 tiles 110.7 us against 195.5 on 128x64)
+  if (tile == 0 && p.m <= 64 && !one_tile) return tiles_64x64(c, amn, bmn);
   // 128x64 tiles that fill (nearly) whole waves of one tile per SM: 256
   // threads of 4x8 beat two 64x64 CTAs per SM by 3-7 % (tools/sgemm_ms_bench.cu:
   // 1024^3 56 -> 53 us, 1536^3 148 -> 143 us; both-K-contiguous layouts lose)
