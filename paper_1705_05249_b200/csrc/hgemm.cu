@@ -148,7 +148,10 @@ int dispatch_hgemm_bn(const Call& c, int pair) {
     // The pair once its CTAs (two per pair tile) fill three quarters of the
     // SMs: 2048^2 x 8192 55.3 us against 61.4 for the single-CTA 128 x 256
     // tiles in the same single wave (tools/route_audit.py).
-    const bool two_sm = pair < 0 ? (BN == 256 && !(c.flags & TB_FLAG_NO_2SM) && 8 * pair_tiles >= 3 * sms)
+    // Not for short K: 8192^2 x 256 (4 K blocks) ran 79.9 us on the pair
+    // against 70.7 on the single-CTA 128 x 256 tiles.
+    const bool two_sm = pair < 0 ? (BN == 256 && !(c.flags & TB_FLAG_NO_2SM) && 8 * pair_tiles >= 3 * sms &&
+                                    p.k >= 8 * HG_BK)
                                  : pair >= 1;
     const bool wide = two_sm && pair == 2;
     const bool sync_waves = two_sm && (huge || (c.flags & TB_FLAG_WAVE_SYNC));
@@ -180,15 +183,16 @@ int dispatch_hgemm_bn(const Call& c, int pair) {
 // per-element MMA / reduction sequence).  Doubles while the 128x128 tiles of
 // one instance still leave half the SMs idle and each CTA keeps >= 16 K blocks
 // (measured: 1024^3 with 8 K blocks per CTA was slower split than unsplit),
-// up to KS = 4 for the built-in route (512^2 x 16384: KS 4 30.8 us against
-// KS 8 36.8 — eight partials per tile cost more than the wider spread saves;
-// a gemm_b200 configuration can still ask for 8).
+// and KS = 8 only while KS * tiles stays within a quarter of the SMs (512^2 x
+// 16384, 16 tiles: KS 4 30.8 us against KS 8 36.8 — eight partials per tile
+// cost more than the wider spread saves; 256^2 x 32768, 4 tiles: KS 8 30.8
+// against KS 4 45.0).
 int hgemm_split_ks(const Problem& p) {
   const int sms = sms_or_default();
   const int64_t t1 = ((p.m + HG_BM - 1) / HG_BM) * ((p.n + SK_BN - 1) / SK_BN);
   const int64_t nkb = (p.k + HG_BK - 1) / HG_BK;
   int ks = 1;
-  while (ks < 4 && t1 * ks * 2 <= sms && nkb >= 32 * ks) ks *= 2;
+  while (ks < 8 && t1 * ks * 2 <= sms && nkb >= 32 * ks && (ks < 4 || 4 * t1 * ks <= sms)) ks *= 2;
   return ks;
 }
 

@@ -71,9 +71,9 @@ int big_tiles(const Call& c, bool amn, bool bmn) {
 // KS 2 102.4 / unsplit 86.1; C1 (1024^3, 128 tiles) ties and stays unsplit
 // (split in two measured 59.4 against 55.8 us).
 // Returns 1 when K is not split.
-int sgemm_split_ks(const Problem& p) {
+int sgemm_split_ks(const Problem& p, int bm = 128, int bn = 64) {
   const int sms = sms_or_default();
-  const int64_t t1 = ((p.m + 127) / 128) * ((p.n + 63) / 64);
+  const int64_t t1 = ((p.m + bm - 1) / bm) * ((p.n + bn - 1) / bn);
   const int64_t ktiles = (p.k + 31) / 32;
   if (2 * t1 > sms) return 1;
   int best = 1;
@@ -170,6 +170,19 @@ int dispatch_sgemm_tma(const Call& c, int tile, int mwg, int nwg, int ks) {
   if (tile == 3) return tiles_32x32(c, amn, bmn);
   if (tile == 0 && (amn || bmn) && !(c.flags & TB_FLAG_NO_SPLITK)) {
     const int ks = sgemm_split_ks(p);
+    // Still fewer than half the SMs busy: the 64x32 tiles (four times as
+    // many) split by the same rule — 128^2 x 65536: 325.6 us against 733.2
+    // on the 128x64 split, 256^2 x 32768: 169.8 against 385.1.
+    const int64_t t1 = ((p.m + 127) / 128) * ((p.n + 63) / 64);
+    if (2 * t1 * ks < sms_or_default()) {
+      const int ks32 = sgemm_split_ks(p, 64, 32);
+      const int64_t t32 = ((p.m + 63) / 64) * ((p.n + 31) / 32);
+      if (t32 * ks32 > t1 * ks) {
+        if (ks32 == 2) return tiles_64x32_split<2>(c, amn, bmn);
+        if (ks32 == 4) return tiles_64x32_split<4>(c, amn, bmn);
+        return tiles_64x32(c, amn, bmn);
+      }
+    }
     if (ks == 2) return tiles_128x64_split<2>(c, amn, bmn);
     if (ks == 4) return tiles_128x64_split<4>(c, amn, bmn);
   }

@@ -106,7 +106,7 @@ def _hgemm_split_ks(m: int, n: int, k: int, sms: int) -> int:
     t1 = -(-m // 128) * -(-n // 128)
     nkb = -(-k // 64)
     ks = 1
-    while ks < 4 and t1 * ks * 2 <= sms and nkb >= 32 * ks:
+    while ks < 8 and t1 * ks * 2 <= sms and nkb >= 32 * ks and (ks < 4 or 4 * t1 * ks <= sms):
         ks *= 2
     return ks
 

@@ -22,7 +22,7 @@ NAMES = ("MWG", "NWG", "KWG", "STAGES", "CTA_GROUP", "SPLIT_K", "GROUP_M")
 CASES = [
     # id, prec, m, n, k, batch, gemm_b200 config (or None), flags, expected kernel substring
     ("h_single", "H", 300, 520, 200, 1, None, 0, "hgemm_tc_tma"),
-    ("h_pair", "H", 2304, 2560, 256, 1, None, 0, "2sm"),
+    ("h_pair", "H", 2304, 2560, 512, 1, None, 0, "2sm"),
     ("h_pair512_cfg", "H", 2304, 2600, 256, 1, (256, 512, 64, 0, 2, 1, 0), 0, "256x512"),
     ("h_splitk", "H", 260, 130, 4160, 1, None, 0, "splitk"),
     ("h_splitk_cfg", "H", 300, 200, 1000, 1, (128, 128, 64, 0, 1, 4, 0), 0, "splitk4"),

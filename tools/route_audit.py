@@ -18,7 +18,8 @@ ctx = tb.context_create(tb.host_device())
 flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 clean = torch.ones(256 << 20, dtype=torch.uint8, device="cuda")
 names = ("MWG", "NWG", "KWG", "STAGES", "CTA_GROUP", "SPLIT_K", "GROUP_M")
-precs = sys.argv[1:] or ["H", "S"]
+precs = [a for a in sys.argv[1:] if a in ("H", "S")] or ["H", "S"]
+SET2 = "--set2" in sys.argv
 
 
 def timed(fn, reps):
@@ -42,6 +43,10 @@ SHAPES = [(256, 256, 256), (512, 512, 512), (768, 768, 768), (1024, 1024, 1024),
           (1024, 1024, 8192), (2048, 2048, 8192), (512, 512, 16384), (8192, 256, 1024),
           (256, 8192, 1024), (4096, 512, 4096), (512, 4096, 4096), (16384, 64, 2048),
           (2048, 512, 512), (3000, 2000, 1000)]
+if SET2:
+    SHAPES = [(1000, 1000, 1000), (4000, 1000, 500), (100, 10000, 1000), (6000, 300, 3000), (128, 128, 65536),
+              (8192, 8192, 256), (256, 256, 32768), (12288, 1024, 1024), (1024, 12288, 1024), (2500, 2500, 2500),
+              (5000, 5000, 500), (640, 640, 8192), (96, 4096, 4096), (4096, 96, 4096), (1500, 700, 3000)]
 for p in precs:
     prec = tb.Precision.H if p == "H" else tb.Precision.S
     for (m, n, k) in SHAPES:
