@@ -125,6 +125,11 @@ inline bool aligned_elems(const void* base, int64_t off, int64_t elem, int64_t v
 unsigned int* wave_counter(cudaStream_t stream);
 // Split-K partial workspace of `bytes` for (device, stream), or nullptr (tbgemm.cu).
 void* splitk_workspace(cudaStream_t stream, size_t bytes);
+// Per-(device, stream) growable scratch for repacked operands (tbgemm.cu);
+// nullptr while the stream is capturing a graph and the slot is too small.
+void* pack_workspace(cudaStream_t stream, size_t bytes);
+// Fold `n` more launches into the last launch record and tag its name.
+void note_extra_launches(int n, const char* suffix);
 
 // Dispatchers.
 int dispatch_sgemm(const Call& c);                                   // sgemm.cu

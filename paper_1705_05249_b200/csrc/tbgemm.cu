@@ -209,6 +209,59 @@ void* splitk_workspace(cudaStream_t stream, size_t bytes) {
   return p;
 }
 
+// Repack scratch: one growable buffer per (device, stream), reused in stream
+// order (each call's packs and GEMM are queued on that stream).  Growing
+// frees the old buffer (cudaFree synchronises, so nothing still reads it).
+// Never handed out while the stream is capturing a graph: a captured graph
+// would keep the pointer past a later growth.
+struct PackPool {
+  cudaStream_t streams[kWsSlots] = {};
+  void* ptr[kWsSlots] = {};
+  size_t bytes[kWsSlots] = {};
+  int used = 0;
+};
+static std::mutex g_pack_mu;
+static PackPool g_pack[64];
+
+void* pack_workspace(cudaStream_t stream, size_t bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lock(g_pack_mu);
+  PackPool& pp = g_pack[dev];
+  int slot = -1;
+  for (int i = 0; i < pp.used; ++i)
+    if (pp.streams[i] == stream) slot = i;
+  if (slot >= 0 && pp.bytes[slot] >= bytes) return pp.ptr[slot];
+  if (slot < 0) {
+    if (pp.used == kWsSlots) return nullptr;
+    slot = pp.used++;
+    pp.streams[slot] = stream;
+  } else if (pp.ptr[slot] != nullptr) {
+    cudaFree(pp.ptr[slot]);
+    pp.ptr[slot] = nullptr;
+    pp.bytes[slot] = 0;
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  pp.ptr[slot] = p;
+  pp.bytes[slot] = bytes;
+  return p;
+}
+
+void note_extra_launches(int n, const char* suffix) {
+  g_last.launches += n;
+  const size_t len = strlen(g_last.kernel);
+  snprintf(g_last.kernel + len, sizeof(g_last.kernel) - len, "%s", suffix);
+}
+
 }  // namespace host
 }  // namespace tb
 

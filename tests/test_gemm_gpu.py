@@ -375,3 +375,37 @@ def test_cta_pair_kernel_bitwise_equals_single_cta(ctx, layout, ta, tbn):
     tol = 4 * 2.0 ** -10 * k * A[rows].abs().amax(1, keepdim=True) * B.abs().amax(0, keepdim=True) \
         + 2.0 ** -11 * want.abs()
     assert bool(((C[rows].double() - want).abs() <= tol).all())
+
+
+@pytest.mark.parametrize("layout", ["row", "col"])
+@pytest.mark.parametrize("ta,tbn", [("n", "n"), ("t", "n"), ("n", "t"), ("t", "t")])
+def test_unaligned_h_repacked_equals_ldg_path(ctx, layout, ta, tbn):
+    """H operands with leading dimensions that are not a multiple of 8 are
+    copied once into 16-byte aligned scratch and run on the TMA kernels
+    (hgemm.cu hgemm_repacked, kernel name "+pack"); the values are the
+    operands exactly, so the result equals the LDG-producer path bitwise."""
+    from paper_1705_05249_b200.kernels import native
+    from paper_1705_05249_b200.kernels.dispatch import gemm_native
+
+    m, n, k = 700, 520, 333
+    prec = Precision.H
+    L = Layout.ROW_MAJOR if layout == "row" else Layout.COL_MAJOR
+    rng = np.random.default_rng(m + n + k + len(layout) + ord(ta) + ord(tbn))
+    ar, ac = (k, m) if ta == "t" else (m, k)
+    br, bc = (n, k) if tbn == "t" else (k, n)
+    lda = (ac if layout == "row" else ar) + 3
+    ldb = (bc if layout == "row" else br) + 5
+    ldc = (n if layout == "row" else m) + 1
+    span = lambda r, c, ld: (r - 1) * ld + c if layout == "row" else (c - 1) * ld + r  # noqa: E731
+    a = make_buffer(ctx, rng.uniform(-1, 1, span(ar, ac, lda) + 1).astype(np.float16), prec)
+    b = make_buffer(ctx, rng.uniform(-1, 1, span(br, bc, ldb) + 3).astype(np.float16), prec)
+    outs, kernels = [], []
+    for flags in (0, native.FLAG_NO_TMA):
+        c = tb.buffer_alloc(ctx, prec, span(m, n, ldc))
+        rec = gemm_native(ctx, prec, L, T[ta], T[tbn], m, n, k, 1.0, a, 1, lda, b, 3, ldb, 0.0, c, 0, ldc,
+                          None, flags)
+        outs.append(tb.buffer_read(c, 0, c.length))
+        kernels.append(rec["kernel"])
+    assert kernels[0].endswith("+pack") and "tma" in kernels[0], kernels
+    assert "ldg" in kernels[1], kernels
+    assert outs[0].tobytes() == outs[1].tobytes(), kernels
