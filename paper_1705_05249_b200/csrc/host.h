@@ -130,6 +130,11 @@ void* splitk_workspace(cudaStream_t stream, size_t bytes);
 void* pack_workspace(cudaStream_t stream, size_t bytes);
 // Fold `n` more launches into the last launch record and tag its name.
 void note_extra_launches(int n, const char* suffix);
+// Copy the operands whose pitch / base / stride break 16-byte alignment into
+// scratch with pitches rounded up to 16 bytes (es: element size); c2 is c
+// pointing at the copies.  TB_OK, -1 when not applicable (nothing to copy,
+// per-instance offset arrays, no scratch), or a CUDA error.
+int repack_operands(const Call& c, int es, Call& c2, int& launches);
 
 // Dispatchers.
 int dispatch_sgemm(const Call& c);                                   // sgemm.cu

@@ -184,6 +184,18 @@ int dispatch_sgemm(const Call& c) {
     if (p.batch > 1) vec = vec && (p.stride_a % 4 == 0) && (p.stride_b % 4 == 0);
   }
   if (c.flags & TB_FLAG_SIMT_GENERAL) vec = false;
+  // Unaligned operands (not the testing flag): repack once into aligned
+  // scratch and route the copies (tbgemm.cu repack_operands; 2501^3: 1130
+  // us on the general kernel).
+  if (!vec && !(c.flags & TB_FLAG_SIMT_GENERAL) && !p.a_offs && !p.b_offs) {
+    Call c2 = c;
+    int launches = 0;
+    if (repack_operands(c, 4, c2, launches) == TB_OK) {
+      const int rc = dispatch_sgemm(c2);
+      if (rc == TB_OK) note_extra_launches(launches, "+pack");
+      return rc;
+    }
+  }
   // Every SGEMM instantiation computes the same sequential-k FMA chain per
   // element, so tile choice is free to follow speed.
   if (!vec) return launch_simt<64, 64, 16, 4, 4, false, 2>(c);

@@ -256,6 +256,86 @@ void* pack_workspace(cudaStream_t stream, size_t bytes) {
   return p;
 }
 
+// Unaligned operands: TMA needs 16-byte aligned row pitches and bases; with
+// an odd leading dimension the kernels fall back to per-element loads, an
+// order of magnitude slower for H (2500^3: 1165 us) and ~2x for S.  Copy each
+// offending operand once into the per-stream scratch with its pitch rounded
+// up to 16 bytes (the reference pads its operands too, level3.py:71-82) and
+// run the aligned kernels on the copies: same values, same bits.
+// One thread: one 16-byte vector of a row — element loads from the unaligned
+// source, one 16-byte store into the aligned copy (its pitch is a multiple of
+// the vector and the tail of the last vector lands in the padding).
+template <typename T>
+__global__ void __launch_bounds__(256) pack_rows_kernel(const T* __restrict__ src, int64_t src_ld,
+                                                        int64_t src_stride, T* __restrict__ dst, int64_t dst_ld,
+                                                        int64_t dst_stride, int64_t rows, int64_t cols,
+                                                        int64_t batch) {
+  constexpr int V = 16 / sizeof(T);
+  grid_dep_wait();
+  const int64_t c0 = (static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x) * V;
+  if (c0 >= cols) return;
+  const int nv = cols - c0 < V ? static_cast<int>(cols - c0) : V;
+  for (int64_t z = 0; z < batch; ++z)
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+      const T* s = src + z * src_stride + r * src_ld + c0;
+      T v[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) v[e] = e < nv ? s[e] : T(0);
+      uint4 out;
+      memcpy(&out, v, 16);
+      *reinterpret_cast<uint4*>(dst + z * dst_stride + r * dst_ld + c0) = out;
+    }
+}
+
+int repack_operands(const Call& c, int es, Call& c2, int& launches) {
+  const Problem& p = c.p;
+  if (p.a_offs || p.b_offs) return -1;
+  if (p.m >= (1LL << 31) || p.n >= (1LL << 31) || p.k >= (1LL << 31) || p.batch >= (1LL << 31)) return -1;
+  const int64_t V = 16 / es;
+  // stored (rows, cols) of op(A) / op(B) in the canonical column-major problem
+  const int64_t ar = p.a_kcontig ? p.m : p.k, ac = p.a_kcontig ? p.k : p.m;
+  const int64_t br = p.b_ncontig ? p.k : p.n, bc = p.b_ncontig ? p.n : p.k;
+  const bool pack_a = (p.lda % V) || !aligned_elems(p.a, p.a_off, es, 16) || (p.batch > 1 && (p.stride_a % V));
+  const bool pack_b = (p.ldb % V) || !aligned_elems(p.b, p.b_off, es, 16) || (p.batch > 1 && (p.stride_b % V));
+  if (!pack_a && !pack_b) return -1;
+  const int64_t lda2 = (ac + V - 1) / V * V, ldb2 = (bc + V - 1) / V * V;
+  const int64_t sa2 = ar * lda2, sb2 = br * ldb2;
+  const int64_t bytes = ((pack_a ? p.batch * sa2 : 0) + (pack_b ? p.batch * sb2 : 0)) * es + 64;
+  if (bytes > (int64_t{2} << 30)) return -1;  // at most 2 GB of scratch: otherwise the per-element path
+  uint8_t* next = static_cast<uint8_t*>(pack_workspace(c.stream, static_cast<size_t>(bytes)));
+  if (next == nullptr) return -1;
+  auto pack = [&](const void* base, int64_t off, int64_t ld, int64_t stride, int64_t rows, int64_t cols,
+                  int64_t ld2, int64_t stride2) -> const void* {
+    dim3 grid(static_cast<unsigned>((cols + 256 * V - 1) / (256 * V)), static_cast<unsigned>(rows < 65535 ? rows : 65535));
+    if (es == 4)
+      pack_rows_kernel<uint32_t><<<grid, 256, 0, c.stream>>>(static_cast<const uint32_t*>(base) + off, ld, stride,
+                                                             reinterpret_cast<uint32_t*>(next), ld2, stride2, rows,
+                                                             cols, p.batch);
+    else
+      pack_rows_kernel<uint16_t><<<grid, 256, 0, c.stream>>>(static_cast<const uint16_t*>(base) + off, ld, stride,
+                                                             reinterpret_cast<uint16_t*>(next), ld2, stride2, rows,
+                                                             cols, p.batch);
+    ++launches;
+    const void* out = next;
+    next += (p.batch * stride2 * es + 15) / 16 * 16;
+    return out;
+  };
+  c2 = c;
+  if (pack_a) {
+    c2.p.a = pack(p.a, p.a_off, p.lda, p.stride_a, ar, ac, lda2, sa2);
+    c2.p.a_off = 0;
+    c2.p.lda = lda2;
+    c2.p.stride_a = sa2;
+  }
+  if (pack_b) {
+    c2.p.b = pack(p.b, p.b_off, p.ldb, p.stride_b, br, bc, ldb2, sb2);
+    c2.p.b_off = 0;
+    c2.p.ldb = ldb2;
+    c2.p.stride_b = sb2;
+  }
+  return check_launch("operand repack");
+}
+
 void note_extra_launches(int n, const char* suffix) {
   g_last.launches += n;
   const size_t len = strlen(g_last.kernel);

@@ -85,11 +85,12 @@ def test_padded_leading_dims_and_beta_zero(ctx):
     assert got.tobytes() == want.tobytes()
 
 
-def test_unaligned_ld_falls_back_bitwise(ctx):
-    # lda not a multiple of 4 floats: no tensor map (16-byte strides), the
-    # register-staged kernel runs and still matches bitwise
+def test_unaligned_ld_repacked_bitwise(ctx):
+    # lda not a multiple of 4 floats: no tensor map over the operand as given
+    # (16-byte strides); it is copied once into aligned scratch and the TMA
+    # kernel runs on the copy ("+pack"), still matching bitwise
     got, want, kern = _run(ctx, "col", "n", "n", 257, 190, 131, 1.0, 0.5, 4, a_pad=1)
-    assert not kern.startswith("sgemm_tma_")
+    assert kern.startswith("sgemm_tma_") and kern.endswith("+pack"), kern
     assert got.tobytes() == want.tobytes()
 
 
