@@ -71,8 +71,9 @@ int big_tiles(const Call& c, bool amn, bool bmn) {
 // KS 2 102.4 / unsplit 86.1; C1 (1024^3, 128 tiles) ties and stays unsplit
 // (split in two measured 59.4 against 55.8 us).
 // Returns 1 when K is not split.
-int sgemm_split_ks(const Problem& p, int bm = 128, int bn = 64) {
-  const int sms = sms_or_default();
+int sgemm_split_ks(const Problem& p, int bm = 128, int bn = 64, int per_sm = 1) {
+  // per_sm: CTAs of the tile resident per SM (the 64x32 tiles run several)
+  const int sms = sms_or_default() * per_sm;
   const int64_t t1 = ((p.m + bm - 1) / bm) * ((p.n + bn - 1) / bn);
   const int64_t ktiles = (p.k + 31) / 32;
   if (2 * t1 > sms) return 1;
@@ -168,14 +169,16 @@ int dispatch_sgemm_tma(const Call& c, int tile, int mwg, int nwg, int ks) {
     return -1;
   }
   if (tile == 3) return tiles_32x32(c, amn, bmn);
-  if (tile == 0 && (amn || bmn) && !(c.flags & TB_FLAG_NO_SPLITK)) {
-    const int ks = sgemm_split_ks(p);
+  if (tile == 0 && !(c.flags & TB_FLAG_NO_SPLITK)) {
+    // the 128x64 split kernel needs an M- or N-contiguous operand
+    const int ks = (amn || bmn) ? sgemm_split_ks(p) : 1;
     // Still fewer than half the SMs busy: the 64x32 tiles (four times as
-    // many) split by the same rule — 128^2 x 65536: 325.6 us against 733.2
-    // on the 128x64 split, 256^2 x 32768: 169.8 against 385.1.
+    // many, every layout) split by the same rule — 128^2 x 65536: 325.6 us
+    // against 733.2 on the 128x64 split, 256^2 x 32768: 169.8 against 385.1,
+    // both-K-contiguous 512^2 x 16384: 276 against 412 unsplit.
     const int64_t t1 = ((p.m + 127) / 128) * ((p.n + 63) / 64);
     if (2 * t1 * ks < sms_or_default()) {
-      const int ks32 = sgemm_split_ks(p, 64, 32);
+      const int ks32 = sgemm_split_ks(p, 64, 32, 4);
       const int64_t t32 = ((p.m + 63) / 64) * ((p.n + 31) / 32);
       if (t32 * ks32 > t1 * ks) {
         if (ks32 == 2) return tiles_64x32_split<2>(c, amn, bmn);
@@ -195,6 +198,12 @@ int dispatch_sgemm_tma(const Call& c, int tile, int mwg, int nwg, int ks) {
   const bool one_tile = p.m <= 64 && p.n <= 64;  // batched small instances: one 64x64 tile each
   // (3.5 waves and more: 3072^3 1028 us big tiles against 1091 on 64x64)
   if (tile == 0 && 2 * tiles128 >= 7 * sms && !one_tile) return big_tiles(c, amn, bmn);
+  // K-contiguous A (its tiles are transposed in shared memory either way):
+  // the 64x128 8x8 transposing tiles from one wave of them — 1536^3 NT
+  // 149.5 us against 172.9 on 64x64, 4096x512x4096 NT 374.7 against 438.5
+  // (tools/route_audit.py --trans=nt)
+  const int64_t tiles64x128 = ((p.m + 63) / 64) * ((p.n + 127) / 128) * p.batch;
+  if (tile == 0 && !amn && !one_tile && tiles64x128 >= sms) return big_tiles(c, amn, bmn);
   // fewer 64x64 tiles than SMs (e.g. C3 (64, 3136, 576): 49 tiles): 64x32
   // tiles of 4x4 (21 -> 14 us there; tools/sgemm_ms_bench.cu)
   const int64_t tiles64 = ((p.m + 63) / 64) * ((p.n + 63) / 64) * p.batch;

@@ -20,6 +20,7 @@ clean = torch.ones(256 << 20, dtype=torch.uint8, device="cuda")
 names = ("MWG", "NWG", "KWG", "STAGES", "CTA_GROUP", "SPLIT_K", "GROUP_M")
 precs = [a for a in sys.argv[1:] if a in ("H", "S")] or ["H", "S"]
 SET2 = "--set2" in sys.argv
+TRANS = next((a[len("--trans="):] for a in sys.argv if a.startswith("--trans=")), "nn")
 
 
 def timed(fn, reps):
@@ -54,12 +55,16 @@ for p in precs:
             continue
         a = tb.buffer_from_tensor(ctx, prec, (torch.rand(m * k, device="cuda") * 2 - 1).to(prec.torch_dtype))
         b = tb.buffer_from_tensor(ctx, prec, (torch.rand(k * n, device="cuda") * 2 - 1).to(prec.torch_dtype))
+        ta = tb.Transpose.YES if TRANS[0] == "t" else tb.Transpose.NO
+        tbt = tb.Transpose.YES if TRANS[1] == "t" else tb.Transpose.NO
+        lda = m if TRANS[0] == "t" else k
+        ldb = k if TRANS[1] == "t" else n
         c = tb.buffer_alloc(ctx, prec, m * n)
         reps = 5 if m * n * k > 2 ** 33 else 9
 
         def run(cfg):
-            return lambda: gemm_native(ctx, prec, tb.Layout.ROW_MAJOR, tb.Transpose.NO, tb.Transpose.NO, m, n, k,
-                                       1.0, a, 0, k, b, 0, n, 0.0, c, 0, n, cfg, 0)
+            return lambda: gemm_native(ctx, prec, tb.Layout.ROW_MAJOR, ta, tbt, m, n, k,
+                                       1.0, a, 0, lda, b, 0, ldb, 0.0, c, 0, n, cfg, 0)
         auto_us, auto_k = timed(run(None), reps)
         best = (auto_us, auto_k, "auto")
         for v in b200_variants(prec):
