@@ -71,6 +71,10 @@ template <int BN>
 int launch_hg_tma_stages(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm) {
   constexpr int SHALLOW = BN >= 256 ? 3 : 4;
   if (c.cfg && c.cfg->STAGES == SHALLOW) return launch_hg_layout<BN, true, true, SHALLOW>(c, ta, tbm);
+  // Built-in route, at most 4 K blocks: the shallow ring (the tile's few
+  // stages never fill the deep one; tools/route_audit.py: 128^3 x 1024 26.6
+  // -> 24.6 us, 8192^2 x 256 75.8 -> 70.6 us)
+  if (!(c.cfg && c.cfg->MWG > 0) && c.p.k <= 4 * HG_BK) return launch_hg_layout<BN, true, true, SHALLOW>(c, ta, tbm);
   return launch_hg_layout<BN, true, true>(c, ta, tbm);
 }
 
@@ -151,7 +155,7 @@ int dispatch_hgemm_bn(const Call& c, int pair) {
     // Not for short K: 8192^2 x 256 (4 K blocks) ran 79.9 us on the pair
     // against 70.7 on the single-CTA 128 x 256 tiles.
     const bool two_sm = pair < 0 ? (BN == 256 && !(c.flags & TB_FLAG_NO_2SM) && 8 * pair_tiles >= 3 * sms &&
-                                    p.k >= 8 * HG_BK)
+                                    (p.k + HG_BK - 1) / HG_BK >= 8)
                                  : pair >= 1;
     const bool wide = two_sm && pair == 2;
     const bool sync_waves = two_sm && (huge || (c.flags & TB_FLAG_WAVE_SYNC));
@@ -386,10 +390,17 @@ int dispatch_hgemm(const Call& c) {
   const int sms = sms_or_default();
   auto tiles = [&](int b) { return ((p.m + HG_BM - 1) / HG_BM) * ((p.n + b - 1) / b) * p.batch; };
   auto cost = [&](int b) { return ((tiles(b) + sms - 1) / sms) * b; };
+  // Batched instances too (their N extent is often narrow: 96^3 x 2048
+  // 37.2 us on 128 x 256 against 28.7 on 128 x 128, 384^3 x 64 23.6 -> 20.5);
+  // for them only a clear gain (15 %) narrows the tile (200^3 x 256: 22.5 us
+  // on 128 x 256, 26.7 on 128 x 128 at a 12.5 % smaller wave count).
   int bn = 256;
   if (tiles(256) < sms)
     for (int b = 128; b >= 64; b /= 2)
       if (cost(b) < cost(bn)) bn = b;
+  if (tiles(256) >= sms && p.batch > 1)
+    for (int b = 128; b >= 64; b /= 2)
+      if (20 * cost(b) < 17 * cost(bn)) bn = b;
   if (bn == 256) return dispatch_hgemm_bn<256>(c, -1);
   if (bn == 128) return dispatch_hgemm_bn<128>(c, -1);
   return dispatch_hgemm_bn<64>(c, -1);

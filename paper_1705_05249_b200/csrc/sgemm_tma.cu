@@ -180,16 +180,27 @@ int dispatch_sgemm_tma(const Call& c, int tile, int mwg, int nwg, int ks) {
     if (2 * t1 * ks < sms_or_default()) {
       const int ks32 = sgemm_split_ks(p, 64, 32, 4);
       const int64_t t32 = ((p.m + 63) / 64) * ((p.n + 31) / 32);
-      if (t32 * ks32 > t1 * ks) {
+      if (ks32 > 1 && t32 * ks32 > t1 * ks) {  // unsplit: the routing below (it sees the batch)
         if (ks32 == 2) return tiles_64x32_split<2>(c, amn, bmn);
-        if (ks32 == 4) return tiles_64x32_split<4>(c, amn, bmn);
-        return tiles_64x32(c, amn, bmn);
+        return tiles_64x32_split<4>(c, amn, bmn);
       }
     }
     if (ks == 2) return tiles_128x64_split<2>(c, amn, bmn);
     if (ks == 4) return tiles_128x64_split<4>(c, amn, bmn);
   }
   const int sms = sms_or_default();
+  // Batched instances up to 512 x 512: the tile that pads an instance least,
+  // ties to 64x64, then 128x64, then 32x32 (tools/route_audit.py --batched:
+  // 96^3 x 2048 on 32x32 94 us, 128^3 x 1024 and 256^3 x 256 on 64x64 100
+  // and 180 us, 200^3 x 256 on 32x32 129 us — the big tiles, picked by tile
+  // count alone, ran 125-196 us there).
+  if (tile == 0 && p.batch > 1 && p.m <= 512 && p.n <= 512 && !(p.m <= 64 && p.n <= 64)) {
+    auto padded = [&](int bm, int bn) { return ((p.m + bm - 1) / bm * bm) * ((p.n + bn - 1) / bn * bn); };
+    const int64_t w64 = padded(64, 64), w128 = padded(128, 64), w32 = padded(32, 32);
+    if (w64 <= w128 && w64 <= w32) return tiles_64x64(c, amn, bmn);
+    if ((amn || bmn) && w128 <= w32) return tiles_128x64(c, amn, bmn);
+    return tiles_32x32(c, amn, bmn);
+  }
   const int64_t tiles128 = ((p.m + 127) / 128) * ((p.n + 127) / 128) * p.batch;
   // Measured on B200 (tools/sgemm_ms_bench.cu): with >= 4 waves of 128x128
   // tiles the big tiles win (64x128 8x8 when both operands are M/N-contiguous:

@@ -21,6 +21,7 @@ names = ("MWG", "NWG", "KWG", "STAGES", "CTA_GROUP", "SPLIT_K", "GROUP_M")
 precs = [a for a in sys.argv[1:] if a in ("H", "S")] or ["H", "S"]
 SET2 = "--set2" in sys.argv
 TRANS = next((a[len("--trans="):] for a in sys.argv if a.startswith("--trans=")), "nn")
+BATCHED = "--batched" in sys.argv
 
 
 def timed(fn, reps):
@@ -48,6 +49,34 @@ if SET2:
     SHAPES = [(1000, 1000, 1000), (4000, 1000, 500), (100, 10000, 1000), (6000, 300, 3000), (128, 128, 65536),
               (8192, 8192, 256), (256, 256, 32768), (12288, 1024, 1024), (1024, 12288, 1024), (2500, 2500, 2500),
               (5000, 5000, 500), (640, 640, 8192), (96, 4096, 4096), (4096, 96, 4096), (1500, 700, 3000)]
+if BATCHED:
+    from paper_1705_05249_b200.kernels.dispatch import gemm_strided_batched_native  # noqa: E402
+    for p in precs:
+        prec = tb.Precision.H if p == "H" else tb.Precision.S
+        for (s_, batch) in ((16, 65536), (48, 8192), (96, 2048), (128, 1024), (200, 256), (256, 256), (384, 64)):
+            e = s_ * s_
+            a = tb.buffer_from_tensor(ctx, prec, (torch.rand(e * batch, device="cuda") * 2 - 1).to(prec.torch_dtype))
+            b = tb.buffer_from_tensor(ctx, prec, (torch.rand(e * batch, device="cuda") * 2 - 1).to(prec.torch_dtype))
+            c = tb.buffer_alloc(ctx, prec, e * batch)
+
+            def run(cfg):
+                return lambda: gemm_strided_batched_native(ctx, prec, tb.Layout.ROW_MAJOR, tb.Transpose.NO,
+                                                           tb.Transpose.NO, s_, s_, s_, 1.0, a, 0, s_, e, b, 0, s_, e,
+                                                           0.0, c, 0, s_, e, batch, cfg, 0)
+            auto_us, auto_k = timed(run(None), 7)
+            best = (auto_us, auto_k, "auto")
+            for v in b200_variants(prec):
+                cfg = tb.Configuration.make("gemm_b200", dict(zip(names, v + (0,))))
+                try:
+                    us, kern = timed(run(cfg), 7)
+                except Exception:  # noqa: BLE001
+                    continue
+                if us < best[0]:
+                    best = (us, kern, v)
+            flag = "  <== " if best[0] < 0.95 * auto_us else ""
+            print(f"{p} {s_}^3 x {batch}: auto {auto_us:9.2f} us {auto_k:40s} best {best[0]:9.2f} us {best[1]:40s}"
+                  f" {best[2]}{flag}", flush=True)
+    sys.exit(0)
 for p in precs:
     prec = tb.Precision.H if p == "H" else tb.Precision.S
     for (m, n, k) in SHAPES:
