@@ -290,6 +290,7 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const T* __restrict__ sr
 int repack_operands(const Call& c, int es, Call& c2, int& launches) {
   const Problem& p = c.p;
   if (p.a_offs || p.b_offs) return -1;
+  if (p.m <= 0 || p.n <= 0 || p.k <= 0 || p.batch <= 0) return -1;  // nothing to read
   if (p.m >= (1LL << 31) || p.n >= (1LL << 31) || p.k >= (1LL << 31) || p.batch >= (1LL << 31)) return -1;
   const int64_t V = 16 / es;
   // stored (rows, cols) of op(A) / op(B) in the canonical column-major problem
