@@ -115,7 +115,7 @@ int launch_h2(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm, bool
   }
   // group_m 8: measured best for pair tiles (also with the wave barrier)
   if (int rc = launch_ex("hgemm_tc_2sm launch", kern, grid, block, Cfg::SMEM_BYTES, c.stream, 1, ta, tbm, p,
-                         tiles_m, tiles_n, cfg_group_m(c, 8), total, ctr))
+                         tiles_m, tiles_n, cfg_group_m(c, BNP == 512 ? 16 : 8), total, ctr))
     return rc;
   char name[64];
   snprintf(name, sizeof(name), "hgemm_tc2sm_tma_256x%d_%c%c%s", BNP, AMN ? 'm' : 'k', BMN ? 'n' : 'k',
@@ -157,7 +157,10 @@ int dispatch_hgemm_bn(const Call& c, int pair) {
     const bool two_sm = pair < 0 ? (BN == 256 && !(c.flags & TB_FLAG_NO_2SM) && 8 * pair_tiles >= 3 * sms &&
                                     (p.k + HG_BK - 1) / HG_BK >= 8)
                                  : pair >= 1;
-    const bool wide = two_sm && pair == 2;
+    // Above ~6 TFLOP (wave-barrier calls, power-capped clocks over tens of
+    // ms) the 256 x 512 pair tile: a quarter less L2 traffic buys clock —
+    // 32768^3 51.1-51.8 ms against 54.9-55.5 ms, interleaved A/B runs.
+    const bool wide = two_sm && (pair == 2 || (pair < 0 && huge));
     const bool sync_waves = two_sm && (huge || (c.flags & TB_FLAG_WAVE_SYNC));
     const uint32_t bbox = two_sm ? 128 : BN;
     if (!bmn) rc = make_map(&tbm, B, p.k, p.n, p.batch, p.ldb, p.stride_b, 64, bbox);
