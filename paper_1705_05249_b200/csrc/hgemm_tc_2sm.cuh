@@ -136,6 +136,70 @@ __device__ __forceinline__ void wave_arrive(unsigned int* ctr) {
   asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
 }
 
+// 256 x 512 pair tile epilogue, full tile with beta == 0: one warp's 32 rows
+// x 256 columns.  Phase 1 drains TMEM — the first 64 columns straight into
+// the warp's two 2 KB staging buffers, the other 192 into 96 registers of
+// FP16 pairs (half(alpha * acc), the rounding of epi_store_block's mode 1;
+// the register file caps at 168 per thread with 10 warps) — and arrives on
+// the leader's tempty, so the next tile's MMAs start; phase 2 writes the 32-
+// column blocks as 16-byte vectors of 8 consecutive rows of one column.
+// Staging: column pair j, row r at word j * 32 + (r ^ 4 (j & 1)), conflict-
+// free for the row-per-lane writes and the 8-row reads.
+__device__ __forceinline__ void epi_store_early_release(uint32_t t_row, uint64_t* tempty, uint32_t* stage,
+                                                        __half* cblk, int64_t ldc, float alpha, int lane) {
+  uint32_t h[6][16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {  // 16 columns per tcgen05.ld
+    uint32_t v[16];
+    tmem_ld_32x32b_x16(t_row + i * 16, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const __half2 x = __floats2half2_rn(__fmul_rn(alpha, __uint_as_float(v[2 * jj])),
+                                          __fmul_rn(alpha, __uint_as_float(v[2 * jj + 1])));
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(&x);
+      const int chunk = i >> 1, j = (i & 1) * 8 + jj;
+      if (chunk < 2)
+        stage[chunk * 512 + j * 32 + (lane ^ ((j & 1) << 2))] = w;
+      else
+        h[chunk - 2][j] = w;
+    }
+  }
+  tc_fence_before();
+  mbar_arrive_cluster(tempty, 0);
+  // lane's two items per block: column pair j, rows 8 rg .. 8 rg + 7
+  const int j0 = lane >> 2, j1 = 8 + (lane >> 2), rg = lane & 3;
+  const int r0 = j0 * 32 + ((rg * 8) ^ ((j0 & 1) << 2)), r1 = j1 * 32 + ((rg * 8) ^ ((j1 & 1) << 2));
+  __half* d0 = cblk + static_cast<int64_t>(2 * j0) * ldc + rg * 8;
+  __half* d1 = cblk + static_cast<int64_t>(2 * j1) * ldc + rg * 8;
+  const int64_t step = 32 * ldc;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    uint32_t* buf = stage + (i & 1) * 512;
+    if (i >= 2) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) buf[j * 32 + (lane ^ ((j & 1) << 2))] = h[i - 2][j];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const int r = it ? r1 : r0;
+      const uint4 x0 = *reinterpret_cast<const uint4*>(buf + r);
+      const uint4 x1 = *reinterpret_cast<const uint4*>(buf + (r ^ 4));
+      uint4 lo, hi;  // column 2j / 2j + 1, rows 8 rg .. 8 rg + 7
+      lo.x = __byte_perm(x0.x, x0.y, 0x5410); hi.x = __byte_perm(x0.x, x0.y, 0x7632);
+      lo.y = __byte_perm(x0.z, x0.w, 0x5410); hi.y = __byte_perm(x0.z, x0.w, 0x7632);
+      lo.z = __byte_perm(x1.x, x1.y, 0x5410); hi.z = __byte_perm(x1.x, x1.y, 0x7632);
+      lo.w = __byte_perm(x1.z, x1.w, 0x5410); hi.w = __byte_perm(x1.z, x1.w, 0x7632);
+      __half* dst = it ? d1 : d0;
+      *reinterpret_cast<uint4*>(dst) = lo;
+      *reinterpret_cast<uint4*>(dst + ldc) = hi;
+    }
+    d0 += step;
+    d1 += step;
+  }
+}
+
 template <bool A_MN, bool B_MN, int BNP = 256>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg<BNP>::THREADS, 1)
     hgemm_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Problem p,
@@ -295,6 +359,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg<BNP>::THREADS,
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(acc * 256);
+      if constexpr (BNP == 512) {
+        // One accumulator: the next tile's MMAs wait for this drain.  For
+        // full tiles with beta == 0 read all 256 columns out of TMEM first
+        // (rounded to FP16 exactly as epi_store_block's mode 1 does), give
+        // the accumulator back, then store from registers while the next
+        // tile runs.
+        __half* cw = Cz + n0 * p.ldc + row0;
+        if (!epi.skip_ab && epi.beta == 0.0f && rows_valid >= 32 && n_left >= BNP && (p.ldc & 7) == 0 &&
+            (reinterpret_cast<uintptr_t>(cw) & 15) == 0) {
+          epi_store_early_release(t_row + half * 256, &tempty[acc], reinterpret_cast<uint32_t*>(stage),
+                                  cw + static_cast<int64_t>(half) * 256 * p.ldc, p.ldc, epi.alpha, lane);
+          if (++acc == ACC) { acc = 0; aph ^= 1; }
+          continue;
+        }
+      }
 #pragma unroll 1
       for (int cb = half * (BNP / 64); cb < (half + 1) * (BNP / 64); ++cb) {
         uint32_t v[32];

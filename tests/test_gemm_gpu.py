@@ -377,6 +377,50 @@ def test_cta_pair_kernel_bitwise_equals_single_cta(ctx, layout, ta, tbn):
     assert bool(((C[rows].double() - want).abs() <= tol).all())
 
 
+@pytest.mark.parametrize("ta,tbn", [("n", "n"), ("t", "t")])
+@pytest.mark.parametrize("alpha,beta,ldc_pad", [(1.0, 0.0, 0), (0.75, 0.0, 0), (0.75, 0.5, 0), (1.0, 0.0, 3)])
+def test_pair_256x512_epilogues_bitwise(ctx, ta, tbn, alpha, beta, ldc_pad):
+    """The 256 x 512 CTA-pair tile (gemm_b200 NWG = 512, CTA_GROUP = 2) gives
+    its single accumulator back before storing full beta == 0 tiles
+    (hgemm_tc_2sm.cuh epi_store_early_release); partial tiles, beta != 0 and
+    unaligned ldc take the per-block epilogue.  Every case equals the
+    256 x 256 pair tile bitwise (same K16 sequence, same rounding)."""
+    import torch
+
+    from paper_1705_05249_b200.kernels.dispatch import gemm_native
+
+    m, n, k = 1100, 1300, 320          # ragged in both dimensions: full and partial tiles
+    prec = Precision.H
+    g = torch.Generator(device="cuda").manual_seed(11)
+    at = (torch.rand(m * k, device="cuda", generator=g) * 2 - 1).half()
+    bt = (torch.rand(k * n, device="cuda", generator=g) * 2 - 1).half()
+    c0 = (torch.rand(m * (n + ldc_pad), device="cuda", generator=g) * 2 - 1).half()
+    a, b = tb.buffer_from_tensor(ctx, prec, at), tb.buffer_from_tensor(ctx, prec, bt)
+    lda = k if ta == "n" else m
+    ldb = n if tbn == "n" else k
+    ldc = n + ldc_pad
+    outs, kernels = [], []
+    for nwg in (256, 512):
+        cfg = tb.Configuration.make("gemm_b200", dict(zip(
+            ("MWG", "NWG", "KWG", "STAGES", "CTA_GROUP", "SPLIT_K", "GROUP_M"), (256, nwg, 64, 0, 2, 1, 8))))
+        c = tb.buffer_from_tensor(ctx, prec, c0.clone())
+        rec = gemm_native(ctx, prec, Layout.ROW_MAJOR, T[ta], T[tbn], m, n, k, alpha, a, 0, lda, b, 0, ldb, beta,
+                          c, 0, ldc, cfg, 0)
+        outs.append(c.device_tensor().clone())
+        kernels.append(rec["kernel"])
+    assert "256x256" in kernels[0] and "256x512" in kernels[1], kernels
+    assert torch.equal(outs[0], outs[1]), kernels
+    A = at.view(m, k).double() if ta == "n" else at.view(k, m).t().double()
+    B = bt.view(k, n).double() if tbn == "n" else bt.view(n, k).t().double()
+    want = alpha * (A @ B) + beta * c0.view(m, ldc)[:, :n].double()
+    got = outs[1].view(m, ldc)[:, :n].double()
+    tol = 4 * 2.0 ** -10 * k * A.abs().amax(1, keepdim=True) * B.abs().amax(0, keepdim=True) \
+        + 2.0 ** -10 * want.abs() + 2.0 ** -10
+    assert bool(((got - want).abs() <= tol).all())
+    if ldc_pad:
+        assert torch.equal(outs[1].view(m, ldc)[:, n:], c0.view(m, ldc)[:, n:])
+
+
 @pytest.mark.parametrize("layout", ["row", "col"])
 @pytest.mark.parametrize("ta,tbn", [("n", "n"), ("t", "n"), ("n", "t"), ("t", "t")])
 def test_unaligned_h_repacked_equals_ldg_path(ctx, layout, ta, tbn):
