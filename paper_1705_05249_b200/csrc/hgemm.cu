@@ -157,10 +157,18 @@ int dispatch_hgemm_bn(const Call& c, int pair) {
     const bool two_sm = pair < 0 ? (BN == 256 && !(c.flags & TB_FLAG_NO_2SM) && 8 * pair_tiles >= 3 * sms &&
                                     (p.k + HG_BK - 1) / HG_BK >= 8)
                                  : pair >= 1;
-    // Above ~6 TFLOP (wave-barrier calls, power-capped clocks over tens of
-    // ms) the 256 x 512 pair tile: a quarter less L2 traffic buys clock —
-    // 32768^3 51.1-51.8 ms against 54.9-55.5 ms, interleaved A/B runs.
-    const bool wide = two_sm && (pair == 2 || (pair < 0 && huge));
+    // The 256 x 512 pair tile (a quarter less L2 traffic, which under the
+    // power cap buys clock) above ~6 TFLOP — 32768^3 51.1-51.8 ms against
+    // 54.9-55.5 ms, interleaved A/B runs — and for long K wherever its tile
+    // waves cost no more than the 256 x 256 ones (ceil(tiles / pairs) x N):
+    // idle-start ABBA blocks (tools/pair512_probe.py) 8192^3 686.0 against
+    // 700.4 us, 10240^3 1374 / 1424, 12288^3 2416 / 2527; at K <= 6144 the
+    // tile's exposed prologue / epilogue ate the gain (6144^3 283.4 / 282.5,
+    // 3072^3 49.1 / 47.1).
+    const int64_t wide_tiles = ((p.m + 255) / 256) * ((p.n + 511) / 512) * p.batch;
+    const int64_t pairs = sms / 2 > 0 ? sms / 2 : 1;
+    const bool wide_fits = 2 * ((wide_tiles + pairs - 1) / pairs) <= (pair_tiles + pairs - 1) / pairs;
+    const bool wide = two_sm && (pair == 2 || (pair < 0 && (huge || (p.k >= 7168 && wide_fits))));
     const bool sync_waves = two_sm && (huge || (c.flags & TB_FLAG_WAVE_SYNC));
     const uint32_t bbox = two_sm ? 128 : BN;
     if (!bmn) rc = make_map(&tbm, B, p.k, p.n, p.batch, p.ldb, p.stride_b, 64, bbox);
