@@ -196,3 +196,41 @@ def test_c5_sampled_block(ctx, prec):
         assert sub.tobytes() == np.ascontiguousarray(got.float().cpu().numpy()).tobytes()
     del a, b, c, at, bt
     torch.cuda.empty_cache()
+
+
+def test_headline_8192_route_and_parity(ctx):
+    """The headline workload (HGEMM 8192^3 row-major NN, bench.py's default)
+    runs on the kernel bench.py reports — the 256 x 512 CTA-pair tile — and
+    equals the 256 x 256 pair tile and the single-CTA kernel bitwise; a
+    sampled 64 x 64 block is within tolerance of the float64 product."""
+    import torch
+
+    from paper_1705_05249_b200.kernels import native
+    from paper_1705_05249_b200.kernels.dispatch import gemm_native
+
+    S = 8192
+    g = torch.Generator(device="cuda").manual_seed(81)
+    at = (torch.rand(S * S, device="cuda", generator=g) * 2 - 1).half()
+    bt = (torch.rand(S * S, device="cuda", generator=g) * 2 - 1).half()
+    a, b = tb.buffer_from_tensor(ctx, Precision.H, at), tb.buffer_from_tensor(ctx, Precision.H, bt)
+    pair256 = tb.Configuration.make("gemm_b200", dict(zip(
+        ("MWG", "NWG", "KWG", "STAGES", "CTA_GROUP", "SPLIT_K", "GROUP_M"), (256, 256, 64, 0, 2, 1, 8))))
+    outs, kernels = [], []
+    for cfg, flags in ((None, 0), (pair256, 0), (None, native.FLAG_NO_2SM)):
+        c = tb.buffer_alloc(ctx, Precision.H, S * S)
+        rec = gemm_native(ctx, Precision.H, R, N, N, S, S, S, 1.0, a, 0, S, b, 0, S, 0.0, c, 0, S, cfg, flags)
+        outs.append(c.device_tensor().clone())
+        kernels.append(rec["kernel"])
+        del c
+    assert kernels[0].startswith("hgemm_tc2sm_tma_256x512"), kernels
+    assert "256x256" in kernels[1] and "2sm" not in kernels[2], kernels
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2]), kernels
+    rows = torch.from_numpy(np.sort(np.random.default_rng(18).choice(S, 64, replace=False))).cuda()
+    cols = torch.from_numpy(np.sort(np.random.default_rng(19).choice(S, 64, replace=False))).cuda()
+    A = at.view(S, S)[rows].double()
+    B = bt.view(S, S)[:, cols].double()
+    got = outs[0].view(S, S)[rows][:, cols].double()
+    tol, wide = gpu_tolerance("H", A[None], B[None])
+    assert float(((got - wide[0]).abs() / tol[0]).max()) <= 1.0
+    del outs, a, b, at, bt
+    torch.cuda.empty_cache()
