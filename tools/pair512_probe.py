@@ -1,6 +1,6 @@
 """HGEMM CTA-pair tile 256x256 against 256x512, interleaved, bench protocol
 (L2 flushed, events), plus a bitwise check between the two.  Dev tool.
-usage: python tools/pair512_probe.py [S ...]"""
+usage: python tools/pair512_probe.py [S | MxNxK ...]"""
 import os
 import sys
 import time
@@ -16,20 +16,21 @@ ctx = tb.context_create(tb.host_device())
 prec = tb.Precision.H
 flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 clean = torch.ones(256 << 20, dtype=torch.uint8, device="cuda")
-sizes = [int(x) for x in sys.argv[1:]] or [8192]
-cfgs = {"256x256 g8": (256, 256, 64, 0, 2, 1, 8),
+sizes = [tuple(int(v) for v in x.split("x")) if "x" in x else (int(x),) * 3 for x in sys.argv[1:]] or [(8192,) * 3]
+cfgs = {"route": None, "256x256 g8": (256, 256, 64, 0, 2, 1, 8),
         "256x512 g8": (256, 512, 64, 0, 2, 1, 8)}
 if os.environ.get("PAIR_GROUPS"):  # 256x512 raster group heights instead
     cfgs = {f"256x512 g{g}": (256, 512, 64, 0, 2, 1, int(g)) for g in os.environ["PAIR_GROUPS"].split(",")}
-for S in sizes:
-    a = tb.buffer_from_tensor(ctx, prec, (torch.rand(S * S, device="cuda") * 2 - 1).half())
-    b = tb.buffer_from_tensor(ctx, prec, (torch.rand(S * S, device="cuda") * 2 - 1).half())
-    c = tb.buffer_alloc(ctx, prec, S * S)
+for (M, N, K) in sizes:
+    S = f"{M}x{N}x{K}"
+    a = tb.buffer_from_tensor(ctx, prec, (torch.rand(M * K, device="cuda") * 2 - 1).half())
+    b = tb.buffer_from_tensor(ctx, prec, (torch.rand(K * N, device="cuda") * 2 - 1).half())
+    c = tb.buffer_alloc(ctx, prec, M * N)
 
     def run(cfg):
         conf = None if cfg is None else tb.Configuration.make("gemm_b200", dict(zip(names, cfg)))
-        return gemm_native(ctx, prec, tb.Layout.ROW_MAJOR, tb.Transpose.NO, tb.Transpose.NO, S, S, S, 1.0, a, 0, S,
-                           b, 0, S, 0.0, c, 0, S, conf, 0)
+        return gemm_native(ctx, prec, tb.Layout.ROW_MAJOR, tb.Transpose.NO, tb.Transpose.NO, M, N, K, 1.0, a, 0, K,
+                           b, 0, N, 0.0, c, 0, N, conf, 0)
 
     outs = {}
     for name, cfg in cfgs.items():
@@ -40,7 +41,7 @@ for S in sizes:
     for name, o in outs.items():
         print(f"S={S} {name:12s} bitwise-equal-to-256x256: {torch.equal(o, ref)}", flush=True)
     del outs
-    reps = 20 if S <= 8192 else 8
+    reps = 20 if M * N * K <= 8192 ** 3 else 8
     res = {n: [] for n in cfgs}
     blocks = {n: [] for n in cfgs}
     kern = {}
@@ -71,5 +72,5 @@ for S in sizes:
     for name, v in res.items():
         v.sort()
         med = v[len(v) // 2]
-        print(f"S={S} {name:12s} median {med:10.1f} us  min {v[0]:10.1f}  {2 * S ** 3 / med / 1e6:7.1f} TF  {kern[name]}",
+        print(f"S={S} {name:12s} median {med:10.1f} us  min {v[0]:10.1f}  {2 * M * N * K / med / 1e6:7.1f} TF  {kern[name]}",
               flush=True)
