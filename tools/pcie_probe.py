@@ -50,6 +50,23 @@ def both():
 
 t = timed(h2d)
 print(f"H2D 256 MB: {t:.3f} ms  {256 / 1024 / t * 1e3:.1f} GB/s", flush=True)
+
+
+def h2d_two():
+    cur = torch.cuda.current_stream()
+    s1.wait_stream(cur)
+    s2.wait_stream(cur)
+    half = h_in.numel() // 2
+    with torch.cuda.stream(s1):
+        d_in[:half].copy_(h_in[:half], non_blocking=True)
+    with torch.cuda.stream(s2):
+        d_in[half:].copy_(h_in[half:], non_blocking=True)
+    cur.wait_stream(s1)
+    cur.wait_stream(s2)
+
+
+t = timed(h2d_two)
+print(f"H2D 256 MB as two halves on two streams: {t:.3f} ms  {256 / 1024 / t * 1e3:.1f} GB/s", flush=True)
 t = timed(d2h)
 print(f"D2H 128 MB: {t:.3f} ms  {128 / 1024 / t * 1e3:.1f} GB/s", flush=True)
 t = timed(both)
