@@ -90,6 +90,28 @@ def _storage(arr: np.ndarray, layout) -> np.ndarray:
     raise UsageError("host arrays must be 1-D or 2-D")
 
 
+_SIGNATURES: dict = {}
+_SM_COUNTS: dict = {}
+
+
+def _signature(fn):
+    """inspect.signature, cached (it costs tens of microseconds per call)."""
+    sig = _SIGNATURES.get(fn)
+    if sig is None:
+        sig = _SIGNATURES[fn] = inspect.signature(fn)
+    return sig
+
+
+def _sm_count(device) -> int:
+    import torch
+
+    key = str(device)
+    n = _SM_COUNTS.get(key)
+    if n is None:
+        n = _SM_COUNTS[key] = torch.cuda.get_device_properties(device).multi_processor_count
+    return n
+
+
 def _is_pinned(flat: np.ndarray) -> bool:
     import torch
 
@@ -252,7 +274,7 @@ def _gemm_pipelined(ctx, precision, xfers, bound) -> None:
     if cuttable and units > 1 and k > 0:
         chunks = int(max(1, min(MAX_CHUNKS, units, units * k * precision.elemsize // CHUNK_BYTES)))
         if precision is Precision.H and alpha != 0:
-            sms = torch.cuda.get_device_properties(ctx.torch_device).multi_processor_count
+            sms = _sm_count(ctx.torch_device)
             cm, cn = (n, m) if row else (m, n)          # canonical column-major (m, n)
             size = -(-units // chunks)
             last = units - size * (chunks - 1)
@@ -374,7 +396,7 @@ def netlib_call(routine_id: str, *args, ctx: Context | None = None, **kwargs):
     precision = _PRECISIONS[rid[0]]
     fn, roles = _ROUTINES[rid[1:]]
     ctx = ctx or default_context()
-    bound = inspect.signature(fn).bind(ctx, *args, **kwargs)
+    bound = _signature(fn).bind(ctx, *args, **kwargs)
     bound.apply_defaults()
     layout = bound.arguments.get("layout", Layout.COL_MAJOR)
     flats, views = {}, {}
