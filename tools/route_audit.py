@@ -3,7 +3,7 @@ route and every instantiated gemm_b200 variant (bench protocol: L2 flushed,
 CUDA events, median of a few runs) and print where the built-in route is
 more than 5 % slower than the best variant.
 
-    python tools/route_audit.py [H|S]
+    python tools/route_audit.py [H|S] [--set2] [--trans=nt|tn|tt] [--batched] [--shapes=MxNxK,...]
 """
 import sys
 
@@ -49,6 +49,9 @@ if SET2:
     SHAPES = [(1000, 1000, 1000), (4000, 1000, 500), (100, 10000, 1000), (6000, 300, 3000), (128, 128, 65536),
               (8192, 8192, 256), (256, 256, 32768), (12288, 1024, 1024), (1024, 12288, 1024), (2500, 2500, 2500),
               (5000, 5000, 500), (640, 640, 8192), (96, 4096, 4096), (4096, 96, 4096), (1500, 700, 3000)]
+CUSTOM = next((a[len("--shapes="):] for a in sys.argv if a.startswith("--shapes=")), None)
+if CUSTOM:  # --shapes=MxNxK,MxNxK (no size cap)
+    SHAPES = [tuple(int(v) for v in x.split("x")) for x in CUSTOM.split(",")]
 if BATCHED:
     from paper_1705_05249_b200.kernels.dispatch import gemm_strided_batched_native  # noqa: E402
     for p in precs:
@@ -80,7 +83,7 @@ if BATCHED:
 for p in precs:
     prec = tb.Precision.H if p == "H" else tb.Precision.S
     for (m, n, k) in SHAPES:
-        if prec is tb.Precision.S and m * n * k > 2 ** 35:
+        if prec is tb.Precision.S and m * n * k > 2 ** 35 and not CUSTOM:
             continue
         a = tb.buffer_from_tensor(ctx, prec, (torch.rand(m * k, device="cuda") * 2 - 1).to(prec.torch_dtype))
         b = tb.buffer_from_tensor(ctx, prec, (torch.rand(k * n, device="cuda") * 2 - 1).to(prec.torch_dtype))
