@@ -50,6 +50,8 @@ int big_tiles(const Call& c, bool amn, bool bmn) {
   // K-contiguous operands are transposed in shared memory (XP) so every
   // layout runs the M/N-contiguous fragment loop: 8192^3 row-major NN
   // 59.8 -> 63.9, K-contiguous A 58.9 -> 64.5, both 56.7 -> 58.9 TFLOP/s
+  // (both K-contiguous on the 128 x 128 / 16 x 8 tile: 18.6 -> 24.4 ms at
+  // 8192^3 — two transposed operands per stage; not used)
   if (amn && bmn) return launch_stma<64, 128, 8, 8, 4, true, true>(c);
   if (amn) return launch_stma<128, 128, 16, 8, 2, true, false, true>(c);
   if (bmn) return launch_stma<64, 128, 8, 8, 2, false, true, true>(c);
