@@ -169,7 +169,11 @@ int dispatch_hgemm_bn(const Call& c, int pair) {
     const int64_t pairs = sms / 2 > 0 ? sms / 2 : 1;
     const bool wide_fits = 2 * ((wide_tiles + pairs - 1) / pairs) <= (pair_tiles + pairs - 1) / pairs;
     const bool wide = two_sm && (pair == 2 || (pair < 0 && (huge || (p.k >= 7168 && wide_fits))));
-    const bool sync_waves = two_sm && (huge || (c.flags & TB_FLAG_WAVE_SYNC));
+    // The wave barrier also on the 256 x 512 tile from 4 waves of it: 8192^3
+    // 679.9 against 684.0 us (idle-start ABBA blocks, tools/pair512_probe.py
+    // PAIR_WS=1).
+    const bool sync_waves = two_sm && (huge || (c.flags & TB_FLAG_WAVE_SYNC) ||
+                                       (wide && pair < 0 && wide_tiles >= 4 * pairs));
     const uint32_t bbox = two_sm ? 128 : BN;
     if (!bmn) rc = make_map(&tbm, B, p.k, p.n, p.batch, p.ldb, p.stride_b, 64, bbox);
     else rc = make_map(&tbm, B, p.n, p.k, p.batch, p.ldb, p.stride_b, 64, 64);

@@ -9,6 +9,7 @@ sys.path.insert(0, ".")
 import torch  # noqa: E402
 
 import paper_1705_05249_b200 as tb  # noqa: E402
+from paper_1705_05249_b200.kernels import native  # noqa: E402
 from paper_1705_05249_b200.kernels.dispatch import gemm_native  # noqa: E402
 
 names = ("MWG", "NWG", "KWG", "STAGES", "CTA_GROUP", "SPLIT_K", "GROUP_M")
@@ -19,6 +20,8 @@ clean = torch.ones(256 << 20, dtype=torch.uint8, device="cuda")
 sizes = [tuple(int(v) for v in x.split("x")) if "x" in x else (int(x),) * 3 for x in sys.argv[1:]] or [(8192,) * 3]
 cfgs = {"route": None, "256x256 g8": (256, 256, 64, 0, 2, 1, 8),
         "256x512 g8": (256, 512, 64, 0, 2, 1, 8)}
+if os.environ.get("PAIR_WS"):  # 256x512 g16 with and without the wave barrier
+    cfgs = {"256x512 g16": (256, 512, 64, 0, 2, 1, 16), "256x512 g16 ws": (256, 512, 64, 0, 2, 1, 16, "ws")}
 if os.environ.get("PAIR_GROUPS"):  # 256x512 raster group heights instead
     cfgs = {f"256x512 g{g}": (256, 512, 64, 0, 2, 1, int(g)) for g in os.environ["PAIR_GROUPS"].split(",")}
 for (M, N, K) in sizes:
@@ -28,9 +31,10 @@ for (M, N, K) in sizes:
     c = tb.buffer_alloc(ctx, prec, M * N)
 
     def run(cfg):
-        conf = None if cfg is None else tb.Configuration.make("gemm_b200", dict(zip(names, cfg)))
+        flags = native.FLAG_WAVE_SYNC if cfg is not None and cfg[-1] == "ws" else 0
+        conf = None if cfg is None else tb.Configuration.make("gemm_b200", dict(zip(names, cfg[:7])))
         return gemm_native(ctx, prec, tb.Layout.ROW_MAJOR, tb.Transpose.NO, tb.Transpose.NO, M, N, K, 1.0, a, 0, K,
-                           b, 0, N, 0.0, c, 0, N, conf, 0)
+                           b, 0, N, 0.0, c, 0, N, conf, flags)
 
     outs = {}
     for name, cfg in cfgs.items():
