@@ -113,9 +113,17 @@ int launch_h2(const Call& c, const CUtensorMap& ta, const CUtensorMap& tbm, bool
     if (ctr && cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned int), c.stream) != cudaSuccess)
       return check_launch("wave counter");
   }
+  // The barrier's one-shot timeout: 2 ms for the > 6 TFLOP calls (tens of
+  // ms); below, ~2 pair tiles' time (a 256 x 512 tile at K = 8192 takes
+  // ~0.1 ms), at least 200 us — so a call sharing the SMs with other work
+  // (CTAs not co-resident) loses at most that, once.
+  const double flop = 2.0 * static_cast<double>(p.m) * p.n * p.k * p.batch;
+  const int64_t kscaled = p.k * 200 / 8192;
+  const unsigned int timeout_us =
+      flop > 6e12 ? 2000u : static_cast<unsigned int>(kscaled < 200 ? 200 : (kscaled > 2000 ? 2000 : kscaled));
   // group_m 8: measured best for pair tiles (also with the wave barrier)
   if (int rc = launch_ex("hgemm_tc_2sm launch", kern, grid, block, Cfg::SMEM_BYTES, c.stream, 1, ta, tbm, p,
-                         tiles_m, tiles_n, cfg_group_m(c, BNP == 512 ? 16 : 8), total, ctr))
+                         tiles_m, tiles_n, cfg_group_m(c, BNP == 512 ? 16 : 8), total, ctr, timeout_us))
     return rc;
   char name[64];
   snprintf(name, sizeof(name), "hgemm_tc2sm_tma_256x%d_%c%c%s", BNP, AMN ? 'm' : 'k', BMN ? 'n' : 'k',

@@ -108,14 +108,15 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
 // K = 32768 (16 MB panels, ~18 panels per wave) L2 reuse collapses (ncu: 329 GB
 // DRAM per 32768^3 call; the barrier measured 945 -> 1286 TFLOP/s there).
 // The barrier is advisory: the target never exceeds the tiles every CTA will
-// finish (ragged last wave), and the first wait that exceeds ~2 ms
-// (%globaltimer) — CTAs not co-resident because other work holds SMs —
+// finish (ragged last wave), and the first wait that exceeds the launch's
+// timeout (%globaltimer; 2 ms above 6 TFLOP, ~2 tiles' time below, set by
+// launch_h2) — CTAs not co-resident because other work holds SMs —
 // raises an abandon flag (ctr[1]) that turns the barrier off for every CTA
 // for the rest of the launch, so a shared GPU costs at most one timeout per
 // call, never one per wave.  The launcher also sizes the grid from
 // cudaOccupancyMaxActiveClusters.  Both words are zeroed on the launch stream
 // before every launch.
-__device__ __forceinline__ void wave_wait(unsigned int* ctr, unsigned int target) {
+__device__ __forceinline__ void wave_wait(unsigned int* ctr, unsigned int target, uint64_t timeout_ns) {
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   unsigned int v, off;
@@ -126,7 +127,7 @@ __device__ __forceinline__ void wave_wait(unsigned int* ctr, unsigned int target
     if (off != 0u) return;
     uint64_t t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    if (t1 - t0 > 2000000ull) {
+    if (t1 - t0 > timeout_ns) {
       asm volatile("st.relaxed.gpu.global.u32 [%0], 1;" ::"l"(ctr + 1) : "memory");
       return;
     }
@@ -203,7 +204,8 @@ __device__ __forceinline__ void epi_store_early_release(uint32_t t_row, uint64_t
 template <bool A_MN, bool B_MN, int BNP = 256>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg<BNP>::THREADS, 1)
     hgemm_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Problem p,
-                        int tiles_m, int tiles_n, int group_m, int64_t total_tiles, unsigned int* wave_ctr) {
+                        int tiles_m, int tiles_n, int group_m, int64_t total_tiles, unsigned int* wave_ctr,
+                        unsigned int wave_timeout_us) {
   using C = H2Cfg<BNP>;
   constexpr int STAGES = C::STAGES;
   constexpr int ACC = C::ACC;
@@ -264,7 +266,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2Cfg<BNP>::THREADS,
     const unsigned int full_waves = static_cast<unsigned int>(total_tiles / n_clusters);
     for (int64_t t = cluster_id; t < total_tiles; t += n_clusters, ++wave) {
       if (wave_ctr != nullptr && wave > 0) {
-        if (elect_one()) wave_wait(wave_ctr, min(wave, full_waves) * gridDim.x);
+        if (elect_one()) wave_wait(wave_ctr, min(wave, full_waves) * gridDim.x, 1000ull * wave_timeout_us);
         __syncwarp();
       }
       int64_t z; int mt, nt;

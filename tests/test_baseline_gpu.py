@@ -234,3 +234,29 @@ def test_headline_8192_route_and_parity(ctx):
     assert float(((got - wide[0]).abs() / tol[0]).max()) <= 1.0
     del outs, a, b, at, bt
     torch.cuda.empty_cache()
+
+
+def test_wave_barrier_with_an_sm_held_by_other_work(ctx):
+    """The wave barrier (on for the 8192^3 256 x 512 route) assumes every
+    CTA pair is co-resident.  With one SM held by a spinning kernel on
+    another stream, one pair starts late: the barrier's one-shot timeout
+    turns it off for the launch, and the result is still bitwise the
+    result of an unshared call (hgemm_tc_2sm.cuh wave_wait)."""
+    import torch
+
+    S = 8192
+    g = torch.Generator(device="cuda").manual_seed(82)
+    at = (torch.rand(S * S, device="cuda", generator=g) * 2 - 1).half()
+    bt = (torch.rand(S * S, device="cuda", generator=g) * 2 - 1).half()
+    a, b = tb.buffer_from_tensor(ctx, Precision.H, at), tb.buffer_from_tensor(ctx, Precision.H, bt)
+    c_ref, c_shared = tb.buffer_alloc(ctx, Precision.H, S * S), tb.buffer_alloc(ctx, Precision.H, S * S)
+    tb.gemm(ctx, R, N, N, S, S, S, 1.0, a, b, 0.0, c_ref)
+    assert ctx.last_launch.native["kernel"].endswith("_ws"), ctx.last_launch.native["kernel"]
+    torch.cuda.synchronize()
+    hog, work = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(hog):
+        torch.cuda._sleep(10_000_000)          # one CTA spinning ~5 ms
+    with torch.cuda.stream(work):
+        tb.gemm(ctx, R, N, N, S, S, S, 1.0, a, b, 0.0, c_shared)
+    torch.cuda.synchronize()
+    assert torch.equal(c_shared.device_tensor(), c_ref.device_tensor())
