@@ -43,7 +43,7 @@ def gemm(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Transpose,
          b_offset: int = 0, ldb: int | None = None,
          c_offset: int = 0, ldc: int | None = None,
          kernel: str | None = None, tf32: bool = False,
-         _config_args: tuple | None = None, _validate_only: bool = False):
+         _config_args: tuple | None = None, _validate_only: bool = False, _flags: int = 0):
     """C = alpha * op(A) op(B) + beta * C on the GPU (asynchronous on the
     context's stream; read results with ``buffer_read`` / ``Buffer.data``).
 
@@ -59,7 +59,8 @@ def gemm(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Transpose,
     configuration of the whole problem; ``_validate_only`` (internal: the
     netlib layer validates the whole call before its first copy) runs every
     check and returns False for the m == 0 / n == 0 no-op, True otherwise,
-    without launching.
+    without launching; ``_flags`` (internal: the same layer's sub-blocks) adds
+    native launch flags (TB_FLAG_NO_SPLITK).
     """
     precision = a.precision
     check_precision(ctx, precision, a, b, c)
@@ -102,5 +103,5 @@ def gemm(ctx: Context, layout: Layout, trans_a: Transpose, trans_b: Transpose,
     kcfg = b200_config(store, precision, ctx.device, shape)
     launched = gemm_native(ctx, precision, layout, trans_a, trans_b, m, n, k, alpha,
                            a, a_offset, lda, b, b_offset, ldb, beta, c, c_offset, ldc, kcfg,
-                           route_flags(kernel) | (native.FLAG_TF32 if tf32 else 0))
+                           route_flags(kernel) | (native.FLAG_TF32 if tf32 else 0) | _flags)
     record_launch(ctx, family, cfg, grid, launched, kcfg)

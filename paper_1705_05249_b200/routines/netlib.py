@@ -23,10 +23,12 @@ streams (H2D copy engine, the context's compute stream, D2H copy engine):
   unchanged, as in the reference.
 
 Every sub-block runs the kernel configuration resolved for the WHOLE problem
-(``gemm(..., _config_args=)``), and an HGEMM is cut only when neither the
+(``gemm(..., _config_args=)``); an HGEMM is cut only when neither the
 whole problem nor a sub-block would take the cluster split-K route (whose
-reduction order depends on the call's shape — hgemm.cu hgemm_split_ks), so
-the result equals the single device call bitwise.
+reduction order depends on the call's shape — hgemm.cu hgemm_split_ks), an
+SGEMM only when its whole problem cannot split (sgemm_tma.cu sgemm_split_ks)
+and its sub-blocks then run unsplit (TB_FLAG_NO_SPLITK), so the result
+equals the single device call bitwise.
 """
 
 from __future__ import annotations
@@ -38,6 +40,7 @@ import numpy as np
 
 from ..core import Context, Layout, Precision, Transpose, buffer_from_tensor, context_create, host_device
 from ..errors import UsageError
+from ..kernels import native
 from . import extras, level3
 from .common import default_ld, stored_dims
 
@@ -273,6 +276,15 @@ def _gemm_pipelined(ctx, precision, xfers, bound) -> None:
     chunks = 1
     if cuttable and units > 1 and k > 0:
         chunks = int(max(1, min(MAX_CHUNKS, units, units * k * precision.elemsize // CHUNK_BYTES)))
+        if precision is Precision.S and alpha != 0:
+            # The S route splits K only with at most half the SMs' worth of
+            # 128 x 64 tiles (sgemm_tma.cu sgemm_split_ks / the 64 x 32 split):
+            # cut only a call whose whole problem cannot split, and run its
+            # sub-blocks unsplit (FLAG_NO_SPLITK) — every unsplit S kernel
+            # runs the same sequential-k chains, so bitwise the whole call.
+            cm, cn = (n, m) if row else (m, n)          # canonical column-major (m, n)
+            if 2 * (-(-cm // 128)) * (-(-cn // 64)) <= _sm_count(ctx.torch_device):
+                chunks = 1
         if precision is Precision.H and alpha != 0:
             sms = _sm_count(ctx.torch_device)
             cm, cn = (n, m) if row else (m, n)          # canonical column-major (m, n)
@@ -310,7 +322,7 @@ def _gemm_pipelined(ctx, precision, xfers, bound) -> None:
         slot_events[slot] = ev_in
         cur.wait_event(ev_in)
         common = dict(lda=lda, ldb=ldb, ldc=ldc, kernel=args.get("kernel"), tf32=args.get("tf32", False),
-                      _config_args=(m, n, k))
+                      _config_args=(m, n, k), _flags=native.FLAG_NO_SPLITK if chunks > 1 else 0)
         if row:
             level3.gemm(ctx, layout, ta, tb, size, n, k, alpha, A.buf, B.buf, beta, C.buf,
                         a_offset=a_off + u0 * lda, b_offset=b_off, c_offset=c_off + u0 * ldc, **common)

@@ -114,6 +114,25 @@ def test_pipelined_hgemm_split_shapes_stay_bitwise(ctx, monkeypatch):
     assert c_host.tobytes() == tb.buffer_read(c, 0, m * n).tobytes()
 
 
+@pytest.mark.parametrize("shape", [(4096, 128, 9216), (2048, 2048, 1024), (64, 3136, 576)])
+def test_pipelined_sgemm_split_shapes_stay_bitwise(ctx, monkeypatch, shape):
+    """SGEMM: a call whose whole problem may take a split-K route (C3
+    (4096, 128, 9216) splits in two) is not cut; a cut call's sub-blocks run
+    unsplit, as its whole problem does.  Bitwise the device call either way."""
+    monkeypatch.setattr(netlib, "CHUNK_BYTES", 1 << 16)
+    prec = Precision.S
+    m, n, k = shape
+    rng = np.random.default_rng(m + n + k)
+    av, bv = _flat(rng, m * k, prec, True), _flat(rng, k * n, prec, True)
+    c_host = np.zeros(m * n, np.float32)
+    tb.netlib_call("sgemm", Layout.ROW_MAJOR, Transpose.NO, Transpose.NO, m, n, k, 1.0, av, bv, 0.0,
+                   c_host, ctx=ctx)
+    a, b = make_buffer(ctx, av, prec), make_buffer(ctx, bv, prec)
+    c = tb.buffer_alloc(ctx, prec, m * n)
+    tb.gemm(ctx, Layout.ROW_MAJOR, Transpose.NO, Transpose.NO, m, n, k, 1.0, a, b, 0.0, c)
+    assert c_host.tobytes() == tb.buffer_read(c, 0, m * n).tobytes()
+
+
 def test_netlib_errors_match_device_routine(ctx):
     """Validation happens on the whole call before any copy, with the device
     routine's errors."""
