@@ -126,6 +126,14 @@ def _is_pinned(flat: np.ndarray) -> bool:
         return False
 
 
+def _sgemm_may_split(m: int, n: int, sms: int) -> bool:
+    """Whether the built-in S route may split K for a (canonical column-
+    major) m x n problem: sgemm_tma.cu sgemm_split_ks returns 1 whenever the
+    128 x 64 tiles fill more than half the SMs, and the 64 x 32 split needs
+    fewer still."""
+    return 2 * (-(-m // 128)) * (-(-n // 64)) <= sms
+
+
 def _hgemm_split_ks(m: int, n: int, k: int, sms: int) -> int:
     """Mirror of hgemm.cu hgemm_split_ks (canonical column-major m, n)."""
     t1 = -(-m // 128) * -(-n // 128)
@@ -283,7 +291,7 @@ def _gemm_pipelined(ctx, precision, xfers, bound) -> None:
             # sub-blocks unsplit (FLAG_NO_SPLITK) — every unsplit S kernel
             # runs the same sequential-k chains, so bitwise the whole call.
             cm, cn = (n, m) if row else (m, n)          # canonical column-major (m, n)
-            if 2 * (-(-cm // 128)) * (-(-cn // 64)) <= _sm_count(ctx.torch_device):
+            if _sgemm_may_split(cm, cn, _sm_count(ctx.torch_device)):
                 chunks = 1
         if precision is Precision.H and alpha != 0:
             sms = _sm_count(ctx.torch_device)

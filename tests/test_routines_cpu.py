@@ -105,3 +105,22 @@ def test_netlib_rejects_unknown_ids():
         tb.netlib_call("xgemm")
     with pytest.raises(tb.UsageError, match="not part of the B200 GEMM path"):
         tb.netlib_call("daxpy")
+
+
+def test_netlib_split_predicates_mirror_the_native_rules():
+    """The host-side mirrors netlib uses to decide whether a call may be cut
+    (sub-blocks must take the same split-K decision as the whole call):
+    hgemm.cu hgemm_split_ks and the S route's split eligibility on 148 SMs."""
+    from paper_1705_05249_b200.routines import netlib
+
+    # H: canonical column-major (m, n); C3 (4096, 128, 9216) row-major is (128, 4096)
+    assert netlib._hgemm_split_ks(128, 4096, 9216, 148) == 4
+    assert netlib._hgemm_split_ks(8192, 8192, 8192, 148) == 1
+    assert netlib._hgemm_split_ks(512, 512, 16384, 148) == 4      # KS 8 only within a quarter of the SMs
+    assert netlib._hgemm_split_ks(256, 256, 32768, 148) == 8
+    assert netlib._hgemm_split_ks(1024, 1024, 1024, 148) == 1     # fewer than 32 K blocks per rank
+    # S: may split only with at most half the SMs' worth of 128 x 64 tiles
+    assert netlib._sgemm_may_split(128, 4096, 148)                # C3: 64 tiles
+    assert netlib._sgemm_may_split(3136, 64, 148)                 # C3b: 25 tiles
+    assert not netlib._sgemm_may_split(1024, 1024, 148)           # C1: 128 tiles
+    assert not netlib._sgemm_may_split(8192, 8192, 148)
